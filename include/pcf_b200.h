@@ -1,0 +1,132 @@
+/* pcf_b200.h -- C ABI of the B200 rectangle-iteration engine (libpcfb200.so).
+ *
+ * This is the drop-in boundary for the reference's kernel plugin.  The reference
+ * selects a kernel module through pcflib._backend._Backend
+ * (pkg/src/pcflib/_backend.py:25-49), whose three calls map onto this ABI as follows:
+ *
+ *   _Backend.integrate_pair(f, g, a, b, op, p)  _backend.py:31-38 -> pcf_integrate_pair_host
+ *       (= _sweepkern.integrate_pair, _sweepkern.pyx:62-69)
+ *   _Backend.pack(collection)                   _backend.py:40-41 -> pcf_pack_sorted (device)
+ *       (= _sweepkern.pack, _sweepkern.pyx:72-85; host concat stays in the caller)
+ *   _Backend.fill_block(packed, r0, r1, ...)    _backend.py:43-46 -> pcf_fill_rows (device) /
+ *       pcf_fill_block_host (host buffers)     (= _sweepkern.fill_block, pyx:88-121)
+ *
+ * plus the whole-matrix path the GPU needs (MatrixJob.run's block loop,
+ * pkg/src/pcflib/matrix.py:156-234, moved on-device): pcf_plan_pairwise + pcf_fill_matrix,
+ * and the reduction path that has no boundary in the reference (reduce.py:31-63,189-238):
+ * pcf_tree_level / pcf_scale_minimize / pcf_moments_level.
+ *
+ * Conventions
+ *  - All functions return PCF_OK (0) or an error code; pcf_last_error() gives the text.
+ *    Nothing throws across the ABI.
+ *  - "_dev" pointers are CUDA device pointers; `stream` is a cudaStream_t (NULL = legacy
+ *    default).  Device-pointer entry points never allocate and never synchronise.
+ *  - "_host" entry points take host arrays, allocate/free device memory internally and
+ *    synchronise before returning (the reference's calling convention).
+ *  - op: PCF_OP_LP (h = |x-y|^p) or PCF_OP_INNER (h = x*y): same codes as
+ *    _sweepkern.OP_LP / OP_INNER (pyx:14-15).
+ *  - Records: one PCF with rows (t_k, v_k), k < n, is n 16-byte records
+ *    {double t_next, double v}; t_next = t_{k+1}, +inf for the last.  Collections are
+ *    concatenated in size-sorted (descending) order with int64 offsets `soff`.
+ *  - err_dev: one unsigned 64-bit word initialised by the caller to UINT64_MAX; receives
+ *    atomicMin(i*M + j) of the first (row-major, original indices, i <= j) non-finite
+ *    entry, i.e. the pair the reference's serial fill_block would report (pyx:109-112).
+ */
+#ifndef PCF_B200_H
+#define PCF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCF_OK 0
+#define PCF_ERR_ARG 1
+#define PCF_ERR_CUDA 2
+#define PCF_ERR_NOMEM 3
+#define PCF_ERR_NONFINITE 4
+
+#define PCF_OP_LP 0
+#define PCF_OP_INNER 1
+
+/* One work item of the pairwise tile scheduler (32 bytes, device-resident array). */
+typedef struct pcf_work_item {
+  int32_t row0;      /* first size-sorted row of the row block */
+  int32_t nrows;     /* R: rows in the block */
+  int32_t col0;      /* first size-sorted column of this item */
+  int32_t col1;      /* one past the last column */
+  int32_t logC;      /* columns per streamed chunk = 1 << logC */
+  int32_t log2G;     /* lanes per pair = 1 << log2G (merge-path split) */
+  int32_t smem_mode; /* 1: operands staged in shared memory, 0: read from L1/L2 */
+  int32_t cost_hi;   /* estimated cells / 2^20 (scheduling order only) */
+} pcf_work_item;
+
+const char* pcf_version(void);
+const char* pcf_last_error(void);
+/* Threads per CTA the tile kernels are compiled for. */
+int pcf_tile_threads(void);
+
+/* ---- K3 sort-pack: reference pack() output (original order) -> sorted records ---- */
+/* tcat/vcat: float32 (is_f32=1) or float64 SoA concatenations, off: int64[M+1] original
+ * offsets, perm: int32[M] sorted->original, soff: int64[M+1] sorted offsets,
+ * recs: 16*soff[M] bytes. */
+int pcf_pack_sorted(const void* tcat_dev, const void* vcat_dev, int is_f32,
+                    const int64_t* off_dev, const int32_t* perm_dev, const int64_t* soff_dev,
+                    int64_t M, void* recs_dev, void* stream);
+
+/* ---- planner (host): sizes in sorted order -> work items, cost-descending ---- */
+/* Returns the dynamic shared memory the items need in *smem_bytes.  `items` may be NULL
+ * to query the count.  max_cols bounds the columns per item (load-balance granularity).
+ * max_log2G caps the merge-path split: 0 = one lane per pair everywhere, which sums every
+ * entry strictly left to right exactly like the reference (bitwise for p=1 and INNER);
+ * 5 = up to a warp per pair (fastest; same cell products, summed in G runs). */
+int pcf_plan_pairwise(const int64_t* sizes_sorted, int64_t M, int64_t smem_budget,
+                      int64_t max_cols, int32_t max_log2G, pcf_work_item* items, int64_t cap,
+                      int64_t* n_items, int32_t* smem_bytes);
+
+/* ---- K1: whole upper triangle (diagonal excluded) of the pairwise matrix ---- */
+/* out_dev: M x M row-major (leading dim ld) float64 (out_is_f32=0) or float32; entries
+ * (perm[p], perm[q]) and mirror are written for every pair covered by items
+ * [0, n_items).  counter_dev: int32 initialised to 0.  p: Lp exponent (ignored for
+ * INNER).  apply_root: r = x^(1/p) as in pdist.  b may be +inf. */
+int pcf_fill_matrix(const void* recs_dev, const int64_t* soff_dev, const int32_t* perm_dev,
+                    int64_t M, const pcf_work_item* items_dev, int64_t n_items,
+                    int32_t smem_bytes, int32_t smem_mode, int32_t* counter_dev, int op,
+                    double p, int apply_root, double a, double b, void* out_dev,
+                    int out_is_f32, int64_t ld, unsigned long long* err_dev, void* stream);
+
+/* Diagonal: Gram <f,f> (gram=1) or exact zeros for distances (gram=0). */
+int pcf_fill_diagonal(const void* recs_dev, const int64_t* soff_dev, const int32_t* perm_dev,
+                      int64_t M, int gram, double a, double b, void* out_dev, int out_is_f32,
+                      int64_t ld, unsigned long long* err_dev, void* stream);
+
+/* ---- fill_block mirror on device: rows [r0, r1) (original order), j > i (j >= i with
+ * diag), written to a compact (r1-r0) x M slab.  inv_dev: original->sorted. ---- */
+int pcf_fill_rows(const void* recs_dev, const int64_t* soff_dev, const int32_t* inv_dev,
+                  int64_t M, int64_t r0, int64_t r1, int op, double p, int apply_root,
+                  int diag, double a, double b, void* slab_dev, int out_is_f32,
+                  unsigned long long* err_dev, void* stream);
+
+/* Raw integrals (no root) of explicit sorted-index pairs; +-inf on divergence. */
+int pcf_pair_list(const void* recs_dev, const int64_t* soff_dev, const int64_t* pairs_dev,
+                  int64_t npairs, int op, double p, double a, double b, double* res_dev,
+                  void* stream);
+
+/* ---- host-buffer mirrors of the reference kernel module (synchronous) ---- */
+/* _sweepkern.integrate_pair (pyx:62-69): raw integral, +-inf on divergence. */
+int pcf_integrate_pair_host(const double* ft, const double* fv, int64_t nf, const double* gt,
+                            const double* gv, int64_t ng, double a, double b, int op, double p,
+                            double* result);
+/* _sweepkern.fill_block (pyx:88-121) on host arrays: tcat/vcat/off = pack() output
+ * (float64), out = host M x M (ld) float64, rows [r0,r1).  *err_i/*err_j = -1 or the
+ * first non-finite pair. */
+int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* off, int64_t M,
+                        int64_t r0, int64_t r1, int op, double p, int apply_root, int diag,
+                        double a, double b, double* out, int64_t ld, int64_t* err_i,
+                        int64_t* err_j);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCF_B200_H */

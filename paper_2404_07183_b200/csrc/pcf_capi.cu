@@ -1,0 +1,378 @@
+// C-ABI layer: argument checking, error text, the tile planner and the host-buffer
+// mirrors of the reference kernel module.  No exceptions cross this boundary.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <algorithm>
+#include <vector>
+#include "pcf_internal.h"
+
+namespace pcfb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static int cuda_fail(cudaError_t e, const char* where) {
+  set_error("%s: %s", where, cudaGetErrorString(e));
+  return PCF_ERR_CUDA;
+}
+
+static int num_sms_current() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return n > 0 ? n : 148;
+}
+
+}  // namespace pcfb
+
+using namespace pcfb;
+
+extern "C" {
+
+const char* pcf_version(void) { return "pcfb200 0.1.0 (sm_100a)"; }
+const char* pcf_last_error(void) { return g_err; }
+int pcf_tile_threads(void) { return kTileThreads; }
+
+int pcf_pack_sorted(const void* tcat_dev, const void* vcat_dev, int is_f32,
+                    const int64_t* off_dev, const int32_t* perm_dev, const int64_t* soff_dev,
+                    int64_t M, void* recs_dev, void* stream) {
+  if (M < 0 || (M > 0 && (!tcat_dev || !vcat_dev || !off_dev || !perm_dev || !soff_dev || !recs_dev))) {
+    set_error("pcf_pack_sorted: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  if (M == 0) return PCF_OK;
+  cudaError_t e = launch_pack(tcat_dev, vcat_dev, is_f32, off_dev, perm_dev, soff_dev, M, recs_dev,
+                              (cudaStream_t)stream);
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_pack_sorted");
+}
+
+// ------------------------------------------------------------------------------ planner
+// Row blocks of the size-sorted collection get the smallest merge-path split G (lanes per
+// pair) whose tile (R resident rows + two streamed chunks of C columns, R*C*G = CTA
+// threads) fits the shared-memory budget.  Column ranges are cut into items of at most
+// max_cols columns; items are returned cost-descending (LPT order for the persistent
+// kernel's atomic queue), shared-memory items first, then global-memory items.
+int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int64_t max_cols,
+                      int32_t max_log2G, pcf_work_item* items, int64_t cap, int64_t* n_items,
+                      int32_t* smem_bytes) {
+  if (M < 0 || (M > 0 && !sizes) || !n_items || smem_budget <= 0) {
+    set_error("pcf_plan_pairwise: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  std::vector<int64_t> S(M + 1, 0);
+  for (int64_t i = 0; i < M; ++i) {
+    if (sizes[i] < 1 || (i > 0 && sizes[i] > sizes[i - 1])) {
+      set_error("pcf_plan_pairwise: sizes must be >= 1 and sorted descending");
+      return PCF_ERR_ARG;
+    }
+    S[i + 1] = S[i] + sizes[i];
+  }
+  auto al = [](int64_t x) { return (x + 127) & ~(int64_t)127; };
+  const int T = kTileThreads;
+  std::vector<pcf_work_item> smem_items, glob_items;
+  int64_t need_max = 0;
+  int64_t r0 = 0;
+  if (max_cols < 1) max_cols = 1 << 30;
+  while (r0 < M - 1) {
+    int sel_logG = -1, sel_logC = 0, sel_R = 0;
+    int64_t sel_need = 0;
+    if (max_log2G < 0) max_log2G = 0;
+    if (max_log2G > 5) max_log2G = 5;
+    for (int logG = 0; logG <= max_log2G && sel_logG < 0; ++logG) {
+      const int P = T >> logG;
+      int best_R = 0, best_logC = 0;
+      int64_t best_need = 0;
+      for (int logC = 0; (1 << logC) <= P; ++logC) {
+        const int C = 1 << logC, R = P >> logC;
+        if (R < C) break;
+        if (R > 4 * C) continue;
+        const int64_t Rr = std::min<int64_t>(R, M - 1 - r0);
+        const int64_t rows_b = (S[r0 + Rr] - S[r0]) * 16;
+        const int64_t c0 = r0 + 1, ce = std::min<int64_t>(c0 + C, M);
+        const int64_t col_b = (S[ce] - S[c0]) * 16;
+        const int64_t need = al(rows_b) + 2 * al(col_b);
+        if (need <= smem_budget && R > best_R) {
+          best_R = R;
+          best_logC = logC;
+          best_need = need;
+        }
+      }
+      if (best_R > 0) {
+        sel_logG = logG;
+        sel_logC = best_logC;
+        sel_R = best_R;
+        sel_need = best_need;
+      }
+    }
+    const bool smem = sel_logG >= 0;
+    if (!smem) {  // PCFs too long to stage: operands from L1/L2, G as large as allowed
+      sel_logG = max_log2G;
+      const int P = T >> sel_logG;  // pairs per pass; square-ish tile R = C or 2C
+      int lc = 0;
+      while ((1 << (2 * (lc + 1))) <= P) ++lc;
+      sel_logC = lc;
+      sel_R = P >> lc;
+    }
+    const int64_t Rr = std::min<int64_t>(sel_R, M - 1 - r0);
+    const int C = 1 << sel_logC;
+    int64_t span = std::max<int64_t>(C, (max_cols / C) * C);
+    const int64_t rows_pts = S[r0 + Rr] - S[r0];
+    for (int64_t c0 = r0 + 1; c0 < M; c0 += span) {
+      const int64_t c1 = std::min<int64_t>(c0 + span, M);
+      pcf_work_item w;
+      w.row0 = (int32_t)r0;
+      w.nrows = (int32_t)Rr;
+      w.col0 = (int32_t)c0;
+      w.col1 = (int32_t)c1;
+      w.logC = sel_logC;
+      w.log2G = sel_logG;
+      w.smem_mode = smem ? 1 : 0;
+      const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;
+      w.cost_hi = (int32_t)std::min(2.0e9, cells / 1048576.0);
+      (smem ? smem_items : glob_items).push_back(w);
+    }
+    if (smem) need_max = std::max(need_max, sel_need);
+    r0 += Rr;
+  }
+  auto by_cost = [](const pcf_work_item& x, const pcf_work_item& y) {
+    return x.cost_hi > y.cost_hi;
+  };
+  std::stable_sort(smem_items.begin(), smem_items.end(), by_cost);
+  std::stable_sort(glob_items.begin(), glob_items.end(), by_cost);
+  const int64_t total = (int64_t)(smem_items.size() + glob_items.size());
+  *n_items = total;
+  if (smem_bytes) *smem_bytes = (int32_t)need_max;
+  if (items) {
+    if (cap < total) {
+      set_error("pcf_plan_pairwise: capacity %lld < %lld items", (long long)cap, (long long)total);
+      return PCF_ERR_ARG;
+    }
+    std::copy(smem_items.begin(), smem_items.end(), items);
+    std::copy(glob_items.begin(), glob_items.end(), items + smem_items.size());
+  }
+  return PCF_OK;
+}
+
+int pcf_fill_matrix(const void* recs_dev, const int64_t* soff_dev, const int32_t* perm_dev,
+                    int64_t M, const pcf_work_item* items_dev, int64_t n_items,
+                    int32_t smem_bytes, int32_t smem_mode, int32_t* counter_dev, int op,
+                    double p, int apply_root, double a, double b, void* out_dev,
+                    int out_is_f32, int64_t ld, unsigned long long* err_dev, void* stream) {
+  if (n_items <= 0) return PCF_OK;
+  if (!recs_dev || !soff_dev || !perm_dev || !items_dev || !counter_dev || !out_dev || !err_dev ||
+      ld < M || (op != PCF_OP_LP && op != PCF_OP_INNER) || !(a >= 0.0) || !(a < b) ||
+      n_items > 0x7fffffff) {
+    set_error("pcf_fill_matrix: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(counter_dev, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return cuda_fail(e, "pcf_fill_matrix memset");
+  FillArgs A;
+  A.recs = recs_dev;
+  A.soff = soff_dev;
+  A.perm = perm_dev;
+  A.M = M;
+  A.items = items_dev;
+  A.n_items = (int)n_items;
+  A.counter = counter_dev;
+  A.op = op;
+  A.p = p;
+  A.a = a;
+  A.b = b;
+  A.apply_root = apply_root;
+  A.out = out_dev;
+  A.out_f32 = out_is_f32;
+  A.ld = ld;
+  A.err = err_dev;
+  A.smem_mode = smem_mode;
+  A.smem_bytes = smem_bytes;
+  A.num_sms = num_sms_current();
+  e = launch_fill_tiles(A, st);
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_fill_matrix");
+}
+
+int pcf_fill_diagonal(const void* recs_dev, const int64_t* soff_dev, const int32_t* perm_dev,
+                      int64_t M, int gram, double a, double b, void* out_dev, int out_is_f32,
+                      int64_t ld, unsigned long long* err_dev, void* stream) {
+  if (M <= 0) return PCF_OK;
+  if (!recs_dev || !soff_dev || !perm_dev || !out_dev || !err_dev || ld < M) {
+    set_error("pcf_fill_diagonal: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  cudaError_t e = launch_diag(recs_dev, soff_dev, perm_dev, M, gram, a, b, out_dev, out_is_f32,
+                              ld, err_dev, (cudaStream_t)stream);
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_fill_diagonal");
+}
+
+int pcf_fill_rows(const void* recs_dev, const int64_t* soff_dev, const int32_t* inv_dev,
+                  int64_t M, int64_t r0, int64_t r1, int op, double p, int apply_root,
+                  int diag, double a, double b, void* slab_dev, int out_is_f32,
+                  unsigned long long* err_dev, void* stream) {
+  if (r1 <= r0) return PCF_OK;
+  if (!recs_dev || !soff_dev || !inv_dev || !slab_dev || !err_dev || r0 < 0 || r1 > M ||
+      (op != PCF_OP_LP && op != PCF_OP_INNER)) {
+    set_error("pcf_fill_rows: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  RowsArgs A;
+  A.recs = recs_dev;
+  A.soff = soff_dev;
+  A.inv = inv_dev;
+  A.M = M;
+  A.r0 = r0;
+  A.r1 = r1;
+  A.op = op;
+  A.p = p;
+  A.a = a;
+  A.b = b;
+  A.apply_root = apply_root;
+  A.diag = diag;
+  A.slab = slab_dev;
+  A.out_f32 = out_is_f32;
+  A.err = err_dev;
+  cudaError_t e = launch_fill_rows(A, (cudaStream_t)stream);
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_fill_rows");
+}
+
+int pcf_pair_list(const void* recs_dev, const int64_t* soff_dev, const int64_t* pairs_dev,
+                  int64_t npairs, int op, double p, double a, double b, double* res_dev,
+                  void* stream) {
+  if (npairs <= 0) return PCF_OK;
+  if (!recs_dev || !soff_dev || !pairs_dev || !res_dev || (op != PCF_OP_LP && op != PCF_OP_INNER)) {
+    set_error("pcf_pair_list: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  cudaError_t e = launch_pair_list(recs_dev, soff_dev, pairs_dev, npairs, op, p, a, b, res_dev,
+                                   (cudaStream_t)stream);
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_pair_list");
+}
+
+// ------------------------------------------------------------------ host-buffer mirrors
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n ? n : 16); }
+};
+}  // namespace
+
+int pcf_integrate_pair_host(const double* ft, const double* fv, int64_t nf, const double* gt,
+                            const double* gv, int64_t ng, double a, double b, int op, double p,
+                            double* result) {
+  if (!ft || !fv || !gt || !gv || !result || nf < 1 || ng < 1) {
+    set_error("pcf_integrate_pair_host: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  const int64_t N = nf + ng;
+  std::vector<double> tc(N), vc(N);
+  std::copy(ft, ft + nf, tc.begin());
+  std::copy(gt, gt + ng, tc.begin() + nf);
+  std::copy(fv, fv + nf, vc.begin());
+  std::copy(gv, gv + ng, vc.begin() + nf);
+  int64_t off[3] = {0, nf, N};
+  int32_t perm[2] = {0, 1};
+  int64_t pairs[2] = {0, 1};
+  DevBuf dt, dv, doff, dperm, drec, dpairs, dres;
+  cudaError_t e;
+  if ((e = dt.alloc(N * 8)) || (e = dv.alloc(N * 8)) || (e = doff.alloc(24)) ||
+      (e = dperm.alloc(8)) || (e = drec.alloc(N * 16)) || (e = dpairs.alloc(16)) ||
+      (e = dres.alloc(8)))
+    return cuda_fail(e, "pcf_integrate_pair_host alloc");
+  cudaMemcpy(dt.p, tc.data(), N * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dv.p, vc.data(), N * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(doff.p, off, 24, cudaMemcpyHostToDevice);
+  cudaMemcpy(dperm.p, perm, 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dpairs.p, pairs, 16, cudaMemcpyHostToDevice);
+  if ((e = launch_pack(dt.p, dv.p, 0, (int64_t*)doff.p, (int32_t*)dperm.p, (int64_t*)doff.p, 2,
+                       drec.p, 0)))
+    return cuda_fail(e, "pcf_integrate_pair_host pack");
+  if ((e = launch_pair_list(drec.p, (int64_t*)doff.p, (int64_t*)dpairs.p, 1, op, p, a, b,
+                            (double*)dres.p, 0)))
+    return cuda_fail(e, "pcf_integrate_pair_host kernel");
+  if ((e = cudaMemcpy(result, dres.p, 8, cudaMemcpyDeviceToHost)))
+    return cuda_fail(e, "pcf_integrate_pair_host copy");
+  return PCF_OK;
+}
+
+int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* off, int64_t M,
+                        int64_t r0, int64_t r1, int op, double p, int apply_root, int diag,
+                        double a, double b, double* out, int64_t ld, int64_t* err_i,
+                        int64_t* err_j) {
+  if (err_i) *err_i = -1;
+  if (err_j) *err_j = -1;
+  if (!tcat || !vcat || !off || !out || M < 1 || r0 < 0 || r1 > M || ld < M) {
+    set_error("pcf_fill_block_host: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  if (r1 <= r0) return PCF_OK;
+  const int64_t N = off[M];
+  std::vector<int32_t> ident(M);
+  for (int64_t i = 0; i < M; ++i) ident[i] = (int32_t)i;
+  const int64_t rows = r1 - r0;
+  DevBuf dt, dv, doff, dperm, drec, dslab, derr;
+  cudaError_t e;
+  if ((e = dt.alloc(N * 8)) || (e = dv.alloc(N * 8)) || (e = doff.alloc((M + 1) * 8)) ||
+      (e = dperm.alloc(M * 4)) || (e = drec.alloc(N * 16)) || (e = dslab.alloc(rows * M * 8)) ||
+      (e = derr.alloc(8)))
+    return cuda_fail(e, "pcf_fill_block_host alloc");
+  cudaMemcpy(dt.p, tcat, N * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dv.p, vcat, N * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(doff.p, off, (M + 1) * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dperm.p, ident.data(), M * 4, cudaMemcpyHostToDevice);
+  cudaMemset(derr.p, 0xff, 8);
+  if ((e = launch_pack(dt.p, dv.p, 0, (int64_t*)doff.p, (int32_t*)dperm.p, (int64_t*)doff.p, M,
+                       drec.p, 0)))
+    return cuda_fail(e, "pcf_fill_block_host pack");
+  RowsArgs A;
+  A.recs = drec.p;
+  A.soff = (int64_t*)doff.p;
+  A.inv = (int32_t*)dperm.p;
+  A.M = M;
+  A.r0 = r0;
+  A.r1 = r1;
+  A.op = op;
+  A.p = p;
+  A.a = a;
+  A.b = b;
+  A.apply_root = apply_root;
+  A.diag = diag;
+  A.slab = dslab.p;
+  A.out_f32 = 0;
+  A.err = (unsigned long long*)derr.p;
+  if ((e = launch_fill_rows(A, 0))) return cuda_fail(e, "pcf_fill_block_host kernel");
+  std::vector<double> slab(rows * M);
+  unsigned long long ekey = ~0ull;
+  if ((e = cudaMemcpy(slab.data(), dslab.p, rows * M * 8, cudaMemcpyDeviceToHost)) ||
+      (e = cudaMemcpy(&ekey, derr.p, 8, cudaMemcpyDeviceToHost)))
+    return cuda_fail(e, "pcf_fill_block_host copy");
+  // The reference stops at the first non-finite entry of the block (row-major) and
+  // leaves the entries after it untouched; mirror that.
+  const int64_t stop_i = ekey == ~0ull ? r1 : (int64_t)(ekey / M);
+  const int64_t stop_j = ekey == ~0ull ? M : (int64_t)(ekey % M);
+  for (int64_t i = r0; i < r1; ++i) {
+    for (int64_t j = i + (diag ? 0 : 1); j < M; ++j) {
+      if (i == stop_i && j == stop_j) goto done;
+      const double x = slab[(i - r0) * M + j];
+      out[i * ld + j] = x;
+      out[j * ld + i] = x;
+    }
+  }
+done:
+  if (ekey != ~0ull) {
+    if (err_i) *err_i = stop_i;
+    if (err_j) *err_j = stop_j;
+  }
+  return PCF_OK;
+}
+
+}  // extern "C"

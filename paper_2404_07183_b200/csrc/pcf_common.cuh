@@ -1,0 +1,113 @@
+// Shared device helpers for the B200 rectangle-iteration engine.
+//
+// Data layout (HBM): every PCF f with stored rows (t_0=0, v_0) .. (t_{n-1}, v_{n-1})
+// is stored as n 16-byte "records"  rec[k] = (t_next = t_{k+1}, v = v_k), with
+// t_next = +inf for the last record.  A record is exactly what one step of the
+// reference sweep (_sweepkern.pyx:38-41) reads for one cursor: the value on the
+// current piece and the time at which that piece ends.  Collections are stored
+// size-sorted (descending) and concatenated, so any run of consecutive PCFs is one
+// contiguous byte range -> one cp.async.bulk copy.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+namespace pcfb {
+
+struct __align__(16) Rec {
+  double t;  // end of this piece (= next breakpoint), +inf on the last piece
+  double v;  // value on this piece
+};
+
+// Integrand kinds.  OP_LP with p=1/2/3 get exact-arithmetic specialisations; any
+// other p goes through pow().  OP_INNER is v_f * v_g.
+enum HKind { H_L1 = 0, H_L2 = 1, H_L3 = 2, H_LP = 3, H_INNER = 4 };
+
+// h(v_f, v_g): _sweepkern.pyx:43-46.  Rounded ops only (no FMA contraction) so the
+// p=1 and inner-product paths reproduce the gcc -O2 (SSE2, no FMA) reference bitwise.
+template <int HK>
+__device__ __forceinline__ double hval(double x, double y, double p) {
+  if (HK == H_L1) return fabs(__dsub_rn(x, y));
+  if (HK == H_L2) {
+    double d = __dsub_rn(x, y);
+    return __dmul_rn(d, d);
+  }
+  if (HK == H_L3) {
+    double d = fabs(__dsub_rn(x, y));
+    return __dmul_rn(__dmul_rn(d, d), d);
+  }
+  if (HK == H_LP) return pow(fabs(__dsub_rn(x, y)), p);
+  return __dmul_rn(x, y);
+}
+
+// ---------------------------------------------------------------- mbarrier / bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk async copy global -> shared (TMA engine, SASS UBLKCP), completion
+// counted in bytes on `bar`.  bytes must be a multiple of 16, both addresses 16B
+// aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Largest count of x in [0, n) with key(x) <= a, for sorted keys (upper_bound).
+template <typename KeyF>
+__device__ __forceinline__ int upper_bound_count(int n, double a, KeyF key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (key(mid) <= a) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double root_p(double acc, double p) {
+  if (p == 1.0) return acc;
+  if (p == 2.0) return sqrt(acc);
+  return pow(acc, 1.0 / p);
+}
+
+template <typename T> __device__ __forceinline__ T cast_out(double x);
+template <> __device__ __forceinline__ double cast_out<double>(double x) { return x; }
+template <> __device__ __forceinline__ float cast_out<float>(double x) { return __double2float_rn(x); }
+
+}  // namespace pcfb

@@ -1,0 +1,61 @@
+// Internal launch interfaces shared by the kernel translation units and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/pcf_b200.h"
+
+namespace pcfb {
+
+constexpr int kTileThreads = 512;  // CTA size of the persistent tile kernels
+
+typedef pcf_work_item PcfWorkItem;
+
+struct FillArgs {
+  const void* recs;
+  const int64_t* soff;
+  const int32_t* perm;
+  int64_t M;
+  const PcfWorkItem* items;
+  int n_items;
+  int* counter;
+  int op;
+  double p, a, b;
+  int apply_root;
+  void* out;
+  int out_f32;
+  int64_t ld;
+  unsigned long long* err;
+  int smem_mode;
+  int smem_bytes;
+  int num_sms;
+};
+
+struct RowsArgs {
+  const void* recs;
+  const int64_t* soff;
+  const int32_t* inv;
+  int64_t M, r0, r1;
+  int op;
+  double p, a, b;
+  int apply_root, diag;
+  void* slab;
+  int out_f32;
+  unsigned long long* err;
+};
+
+int hkind_of(int op, double p);
+cudaError_t launch_fill_tiles(const FillArgs& A, cudaStream_t st);
+cudaError_t launch_diag(const void* recs, const int64_t* soff, const int32_t* perm, int64_t M,
+                        int gram, double a, double b, void* out, int out_f32, int64_t ld,
+                        unsigned long long* err, cudaStream_t st);
+cudaError_t launch_fill_rows(const RowsArgs& A, cudaStream_t st);
+cudaError_t launch_pair_list(const void* recs, const int64_t* soff, const int64_t* pairs,
+                             int64_t npairs, int op, double p, double a, double b, double* res,
+                             cudaStream_t st);
+cudaError_t launch_pack(const void* tcat, const void* vcat, int f32, const int64_t* off,
+                        const int32_t* perm, const int64_t* soff, int64_t M, void* recs,
+                        cudaStream_t st);
+
+void set_error(const char* fmt, ...);
+
+}  // namespace pcfb

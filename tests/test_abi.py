@@ -1,0 +1,119 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports exactly what
+include/pcf_b200.h declares, and the host-side tile planner covers the upper triangle
+exactly once within the shared-memory budget."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+from paper_2404_07183_b200 import _native
+
+HEADER = os.path.join(ROOT, "include", "pcf_b200.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"\b(pcf_[a-z0-9_]+)\s*\(", src))
+
+
+def test_library_loads_and_exports_header():
+    lib = _native.load()
+    declared = header_functions()
+    assert declared == set(_native.SIGNATURES), declared ^ set(_native.SIGNATURES)
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (pcf_[a-z0-9_]+)$", out, flags=re.M))
+    assert declared <= exported, declared - exported
+    for name in declared:
+        assert getattr(lib, name) is not None
+    assert lib.pcf_version().startswith(b"pcfb200")
+    assert lib.pcf_tile_threads() == 512
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def plan(sizes, budget=220 * 1024, max_cols=64, max_log2g=5):
+    lib = _native.load()
+    sizes = np.ascontiguousarray(sizes, dtype=np.int64)
+    n = ctypes.c_int64()
+    smem = ctypes.c_int32()
+    assert lib.pcf_plan_pairwise(_native.ptr(sizes), sizes.shape[0], budget, max_cols, max_log2g,
+                                 None, 0, ctypes.byref(n), ctypes.byref(smem)) == 0
+    items = (_native.WorkItem * max(n.value, 1))()
+    assert lib.pcf_plan_pairwise(_native.ptr(sizes), sizes.shape[0], budget, max_cols, max_log2g,
+                                 ctypes.cast(items, ctypes.c_void_p), n.value, ctypes.byref(n),
+                                 ctypes.byref(smem)) == 0
+    return np.frombuffer(items, dtype=np.int32).reshape(-1, 8)[: n.value].copy(), smem.value
+
+
+@pytest.mark.parametrize("dist", ["appa", "small", "huge", "one", "two"])
+@pytest.mark.parametrize("max_log2g", [0, 5])
+def test_planner_covers_upper_triangle_once(dist, max_log2g):
+    rng = np.random.default_rng(1)
+    sizes = {
+        "appa": rng.integers(10, 1001, 700),
+        "small": rng.integers(1, 30, 900),
+        "huge": np.concatenate([rng.integers(2000, 12000, 20), rng.integers(10, 500, 80)]),
+        "one": np.array([5]),
+        "two": np.array([3, 9]),
+    }[dist]
+    sizes = np.sort(sizes)[::-1].copy()
+    M = sizes.shape[0]
+    items, smem = plan(sizes, max_log2g=max_log2g)
+    seen = np.zeros((M, M), dtype=np.int32)
+    S = np.concatenate([[0], np.cumsum(sizes)])
+    threads = 512
+    for row0, nrows, col0, col1, logc, log2g, mode, cost in items:
+        C, G = 1 << logc, 1 << log2g
+        assert nrows * C * G <= threads
+        assert log2g <= max_log2g
+        assert col0 > row0 and col1 <= M and nrows >= 1
+        if mode == 1:
+            rows_b = (S[row0 + nrows] - S[row0]) * 16
+            col_b = (S[min(col0 + C, col1)] - S[col0]) * 16
+            al = lambda x: (x + 127) // 128 * 128  # noqa: E731
+            assert al(rows_b) + 2 * al(col_b) <= smem <= 220 * 1024
+        for r in range(row0, row0 + nrows):
+            for q in range(col0, col1):
+                if q > r:
+                    seen[r, q] += 1
+    iu = np.triu_indices(M, 1)
+    assert (seen[iu] == 1).all()
+    assert seen.sum() == M * (M - 1) // 2
+    smem_costs = items[items[:, 6] == 1][:, 7]
+    assert (np.diff(smem_costs) <= 0).all()  # LPT order
+
+
+def test_planner_rejects_unsorted():
+    lib = _native.load()
+    sizes = np.array([3, 5], dtype=np.int64)
+    n = ctypes.c_int64()
+    assert lib.pcf_plan_pairwise(_native.ptr(sizes), 2, 1 << 16, 64, 5, None, 0,
+                                 ctypes.byref(n), None) == 1
+    assert b"sorted" in lib.pcf_last_error()
+
+
+def test_no_cuda_means_loud_failure():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2404_07183_b200 as pb
+    from paper_2404_07183_b200 import errors
+
+    fs = [pb.make_pcf([[0, 1], [1, 0]]), pb.make_pcf([[0, 2], [2, 0]])]
+    with pytest.raises(errors.BackendUnavailable):
+        pb.pdist(fs)
+    with pytest.raises(errors.BackendUnavailable):
+        pb.lp_distance(fs[0], fs[1])
