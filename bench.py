@@ -1,0 +1,474 @@
+"""Benchmark: PCF pair-integrals/s of the 100k-PCF L1 distance matrix (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+One step = the full upper triangle of the pairwise L1 distance matrix of M = 100,000
+App-A synthetic PCFs (pcflib.synthetic_benchmark(100000, RngSpec(2404)), float64;
+5.0585e12 rectangle cells, 4.99995e9 pair-integrals) written as the dense M x M result in
+original order.  With N GPUs the cost-sorted tile queue is dealt across ranks (strong
+scaling: the same matrix, 1/N of the pairs per GPU, no collective on the data path).
+
+Printed JSON (rank 0, one line): value = pairs / (max over ranks of the device time of
+K steps) with inputs resident in HBM; e2e = the same metric through the host-buffer
+path (pinned host inputs -> H2D -> device pack -> fill -> D2H of the whole matrix);
+roofline of the dominant kernel (k_fill_tiles_smem) against the FP64 peak measured
+live by a DFMA probe; cpu_baseline = the reference's own compiled kernel
+(oracle/_ref, built from _sweepkern.pyx) on a row sample on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCF pair-integrals/sec (100k-PCF L1 distance matrix)"
+UNIT = "pair-integrals/s"
+FLOPS_PER_CELL_L1 = 4  # |vf - vg|, tn - t, mul, add
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--M", type=int, default=100000)
+    ap.add_argument("--exact", action="store_true", help="one lane per pair (bitwise mode)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(M):
+    from paper_2404_07183_b200 import datagen as dg
+
+    t, v, off = dg.synthetic_benchmark_packed(M, rng=dg.RngSpec(2404))
+    n = np.diff(off)
+    pairs = M * (M - 1) // 2
+    cells = (M - 1) * int(n.sum()) - pairs
+    return t, v, off, pairs, cells
+
+
+# ------------------------------------------------------------------ clocks sampling
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU reference leg
+def cpu_reference_sample(t, v, off, seconds, threads=None):
+    """Time the reference's compiled kernel (oracle/_ref, else the C port) on contiguous
+    row blocks spread over [0, M) with an O(M) aliasing sink, on all host
+    cores.  Returns (pairs/s, cells/s, kind, cores, sample description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from numpy.lib.stride_tricks import as_strided
+
+    M = off.shape[0] - 1
+    threads = threads or os.cpu_count() or 1
+    n = np.diff(off)
+    K = O.load_reference_kernel()
+    kind = "reference" if K is not None else "port"
+    packed = (np.ascontiguousarray(t), np.ascontiguousarray(v), np.ascontiguousarray(off))
+    orc = None if K is not None else O.Oracle()
+    # calibrate: rows spread over [0, M), one row per task
+    rng = np.random.default_rng(0)
+    order = rng.permutation(M - 1)
+    lock = threading.Lock()
+    state = {"next": 0, "pairs": 0, "cells": 0, "stop": False}
+
+    def worker():
+        buf = np.zeros(M)
+        sink = as_strided(buf, shape=(M, M), strides=(0, 8))
+        while True:
+            with lock:
+                if state["stop"] or state["next"] >= order.shape[0]:
+                    return
+                i = int(order[state["next"]])
+                state["next"] += 1
+            if K is not None:
+                K.fill_block(packed, i, i + 1, 0, 1.0, True, False, 0.0, math.inf, sink)
+            else:
+                orc.row(packed[0], packed[1], packed[2], i)
+            np_ = M - 1 - i
+            cl = np_ * (int(n[i]) - 1) + int(off[M] - off[i + 1])
+            with lock:
+                state["pairs"] += np_
+                state["cells"] += cl
+
+    ths = [threading.Thread(target=worker, daemon=True) for _ in range(threads)]
+    t0 = time.perf_counter()
+    for th in ths:
+        th.start()
+    time.sleep(seconds)
+    with lock:
+        state["stop"] = True
+    for th in ths:
+        th.join()
+    dt = time.perf_counter() - t0
+    desc = (f"{state['next']} random rows i of the same {M}-PCF collection, all j > i "
+            f"({state['pairs']} pair-integrals, {state['cells']:.3e} cells) via "
+            f"{'reference _sweepkern.fill_block (oracle/_ref)' if K is not None else 'C port'}"
+            f" on {threads} threads, {dt:.1f} s")
+    return state["pairs"] / dt, state["cells"] / dt, kind, threads, desc
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    M = args.M
+    t, v, off, pairs, cells = workload(M)
+    secs = max(5.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    desc = kind = cores = None
+    for step in range(args.warmup + args.steps):
+        pps, cps, kind, cores, desc = cpu_reference_sample(t, v, off, secs)
+        if step >= args.warmup:
+            vals.append(pps)
+    val = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": pairs / val * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: App-A PCFs (pcflib.synthetic_benchmark, RngSpec(2404))",
+        "config": {"workload": f"c3: L1 distance matrix of {M} App-A PCFs, float64",
+                   "M": M, "pairs": pairs, "cells": cells},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our GPU leg
+def fp64_peak_tflops(lib, torch, stream):
+    from paper_2404_07183_b200 import _native
+
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    iters, bps = 4096, 8
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    for _ in range(2):
+        lib.pcf_probe_fp64(_native.ptr(out), iters, bps, stream)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    lib.pcf_probe_fp64(_native.ptr(out), iters, bps, stream)
+    e.record()
+    torch.cuda.synchronize()
+    flops = nsm * bps * 256 * 8 * iters * 2.0
+    return flops / (s.elapsed_time(e) * 1e-3) / 1e12
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2404_07183_b200 import _native
+    from paper_2404_07183_b200.collection import DeviceCollection, current_stream_handle
+    from paper_2404_07183_b200.engine import (decode_err, item_cells, items_to_device,
+                                              new_err, partition_items)
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    lib = _native.load()
+    M = args.M
+    t, v, off, pairs, cells = workload(M)
+
+    coll = DeviceCollection(t, v, off, device=dev)
+    _, host_items, n_smem, n_glob, smem = coll.plan(exact=args.exact)
+    my_items, my_smem = partition_items(host_items, n_smem, world, rank)
+    my_glob = my_items.shape[0] - my_smem
+    items_dev = items_to_device(my_items, dev)
+    my_cells = item_cells(my_items, coll.sizes_sorted)
+    out = torch.empty((M, M), dtype=torch.float64, device=dev)
+    err = new_err(dev)
+    counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = current_stream_handle()
+    stream = torch.cuda.current_stream()
+
+    ev_k = []
+
+    def step(record=False):
+        lib.pcf_fill_diagonal(_native.ptr(coll.recs), _native.ptr(coll.soff),
+                              _native.ptr(coll.perm), M, 0, 0.0, math.inf, _native.ptr(out), 0,
+                              M, _native.ptr(err), st)
+        launches = 1
+        for lo, cnt, mode in ((0, my_smem, 1), (my_smem, my_glob, 0)):
+            if cnt <= 0:
+                continue
+            if record and mode == 1:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            rc = lib.pcf_fill_matrix(
+                _native.ptr(coll.recs), _native.ptr(coll.soff), _native.ptr(coll.perm), M,
+                _native.c_vp(items_dev.data_ptr() + lo * 32), cnt, smem, mode,
+                _native.ptr(counter), 0, 1.0, 1, 0.0, math.inf, _native.ptr(out), 0, M,
+                _native.ptr(err), st)
+            _native.check(rc, "pcf_fill_matrix")
+            launches += 1
+            if record and mode == 1:
+                b.record(stream)
+                ev_k.append((a, b))
+        return launches
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            launches += step(record=True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        tdist.barrier()
+        ms = float(tt.item())
+    bad = decode_err(err, M)
+    if bad is not None:
+        raise RuntimeError(f"non-finite entry {bad}")
+    value = pairs * args.steps / (ms * 1e-3)
+    kms = [a.elapsed_time(b) for a, b in ev_k]
+    k_avg = float(np.mean(kms)) if kms else float("nan")
+    smem_cells = item_cells(my_items[:my_smem], coll.sizes_sorted)
+    peak = fp64_peak_tflops(lib, torch, st)
+    achieved = FLOPS_PER_CELL_L1 * smem_cells / (k_avg * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tr = json.load(open(tpath))
+            if tr.get("M") == M and tr.get("exact") == bool(args.exact):
+                traffic = tr.get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # ---- end-to-end through the host-buffer path
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, t, v, off, pairs, world, rank, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        pps, cps, kind, cores, desc = cpu_reference_sample(t, v, off, args.cpu_seconds)
+        cpu = {"value": pps, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc,
+               "cells_per_s": cps, "extrapolated_full_matrix_s": cells / cps}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: App-A PCFs (pcflib.synthetic_benchmark(100000, RngSpec(2404)))",
+            "config": {
+                "workload": f"c3: L1 distance matrix of {M} App-A PCFs, float64, full M x M "
+                            "output in original order",
+                "M": M, "pairs": pairs, "cells": cells,
+                "mode": "exact (1 lane/pair)" if args.exact else "fast (merge-path G lanes/pair)",
+                "parallelism": f"tile-queue split over {world} GPU(s)",
+                "l2": "no flush needed: 0.81 GB input records + 80 GB output per step >> 126 MB L2",
+                "work_items": int(host_items.shape[0]), "smem_bytes": smem,
+            },
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "roofline": {
+                "bound": "fp64", "kernel": "k_fill_tiles_smem",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": "measured live: DFMA probe (pcf_probe_fp64); MEASURED_PEAKS.json "
+                               "has no FP64 figure",
+                "algorithmic": f"{FLOPS_PER_CELL_L1} flop/cell x {smem_cells:.4e} cells per launch",
+                "kernel_ms": k_avg,
+                "cells_per_s_per_gpu": smem_cells / (k_avg * 1e-3),
+            },
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def run_e2e(args, t, v, off, pairs, world, rank, dev):
+    """Host-buffer path: pinned inputs -> H2D -> K3 pack -> K1 fill -> D2H of the whole
+    matrix (rank 0 gathers with an NCCL sum-reduce when N > 1; ranks write disjoint
+    entries into zero-initialised buffers, so the sum is exact)."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2404_07183_b200 import _native
+    from paper_2404_07183_b200.collection import DeviceCollection
+    from paper_2404_07183_b200.engine import fill_pairwise, partition_items, items_to_device
+
+    M = off.shape[0] - 1
+    host_t = torch.from_numpy(t).pin_memory()
+    host_v = torch.from_numpy(v).pin_memory()
+    host_off = torch.from_numpy(off).pin_memory()
+    host_out = torch.empty((M, M), dtype=torch.float64, pin_memory=True) if rank == 0 else None
+    out = torch.zeros((M, M), dtype=torch.float64, device=dev) if world > 1 else \
+        torch.empty((M, M), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    bi = host_t.numel() * 8 + host_v.numel() * 8 + host_off.numel() * 8
+    bo = M * M * 8 if rank == 0 else 0
+
+    def e2e_step():
+        coll = DeviceCollection.__new__(DeviceCollection)
+        # same construction as DeviceCollection.__init__, but from pinned host tensors
+        dt = host_t.to(dev, non_blocking=True)
+        dv = host_v.to(dev, non_blocking=True)
+        do = host_off.to(dev, non_blocking=True)
+        _build_collection(coll, dt, dv, do, off, dev)
+        items_dev, host_items, n_smem, n_glob, smem = coll.plan(exact=args.exact)
+        if world > 1:
+            mine, ms_ = partition_items(host_items, n_smem, world, rank)
+            items = (items_to_device(mine, dev), ms_, mine.shape[0] - ms_, smem)
+        else:
+            items = (items_dev, n_smem, n_glob, smem)
+        fill_pairwise(coll, 0, 1.0, True, False, out=out, items=items)
+        if world > 1:
+            tdist.reduce(out, dst=0)
+        if rank == 0:
+            host_out.copy_(out, non_blocking=True)
+
+    for _ in range(1):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    k = max(1, min(args.steps, 2))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(k):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"value": pairs * k / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "ms_per_step": ms / k, "steps": k,
+            "path": "pinned host SoA (reference pack() layout) -> H2D -> pcf_pack_sorted -> "
+                    "pcf_fill_diagonal + pcf_fill_matrix -> D2H of the M x M float64 matrix"}
+
+
+def _build_collection(coll, dt, dv, do, off_host, dev):
+    """DeviceCollection from device-resident SoA arrays (the e2e path)."""
+    import torch
+
+    from paper_2404_07183_b200 import _native
+    from paper_2404_07183_b200.collection import current_stream_handle
+
+    M = off_host.shape[0] - 1
+    sizes = np.diff(off_host)
+    perm = np.argsort(-sizes, kind="stable").astype(np.int32)
+    ssizes = sizes[perm].astype(np.int64)
+    soff = np.zeros(M + 1, dtype=np.int64)
+    np.cumsum(ssizes, out=soff[1:])
+    coll.dtype = np.dtype(np.float64)
+    coll.M = M
+    coll.device = dev
+    coll.sizes_sorted = ssizes
+    coll.perm_host = perm
+    coll.n_points = int(soff[-1])
+    coll.perm = torch.from_numpy(perm).to(dev, non_blocking=True)
+    coll.soff = torch.from_numpy(soff).to(dev, non_blocking=True)
+    coll.inv = None
+    coll.recs = torch.empty(2 * coll.n_points, dtype=torch.float64, device=dev)
+    coll._plans = {}
+    _native.check(_native.load().pcf_pack_sorted(
+        _native.ptr(dt), _native.ptr(dv), 0, _native.ptr(do), _native.ptr(coll.perm),
+        _native.ptr(coll.soff), M, _native.ptr(coll.recs), current_stream_handle()),
+        "pcf_pack_sorted")
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -126,6 +126,44 @@ int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* o
                         double a, double b, double* out, int64_t ld, int64_t* err_i,
                         int64_t* err_j);
 
+/* Dense FP64 FMA throughput probe: nsm*blocks_per_sm CTAs x 256 threads x 8 chains x iters
+ * DFMA (2 flops each); time it with events on `stream` for the FP64 roofline. */
+int pcf_probe_fp64(double* out_dev, int iters, int blocks_per_sm, void* stream);
+
+/* ---- reduction path (mean / std / tree_reduce; pcf_reduce.cu) ----
+ * The reference has no kernel boundary here (reduce.py:31-63,189-238 call the Python
+ * sweep directly); these entry points are the device replacement.  A tree level maps
+ * nodes (SoA times/values, int64 offsets) to output nodes: output k merges input nodes
+ * src[k], src[k]+1 (cnt[k]=2) or passes src[k] through (cnt[k]=1).  Candidates are
+ * written in place of the input positions (st/sv/flag, ntot = input point count), then
+ * pcf_compact scans the keep flags and scatters the kept points.
+ * op: 0 add, 1 max, 2 min, 3 mul (value computed in float64, stored in the kind). */
+int pcf_scan_workspace(int64_t ntot, int64_t* bytes);
+int pcf_level_merge(int op, int is_f32, const void* t_dev, const void* v_dev,
+                    const int64_t* off_dev, const int64_t* src_dev, const int32_t* cnt_dev,
+                    int64_t nout, int64_t ntot, void* st_dev, void* sv_dev, int32_t* flag_dev,
+                    int32_t* status_dev, void* stream);
+/* Parallel-moments (Chan) level for std: per point (mean, M2) in float64, per input node
+ * leaf counts `leaves_dev` (int64). */
+int pcf_level_moments(int is_f32, const void* t_dev, const double* mu_dev, const double* m2_dev,
+                      const int64_t* off_dev, const int64_t* src_dev, const int32_t* cnt_dev,
+                      const int64_t* leaves_dev, int64_t nout, int64_t ntot, void* st_dev,
+                      double* smu_dev, double* sm2_dev, int32_t* flag_dev, void* stream);
+/* value_bytes: element size of sv/sv2 (4 or 8); sv2 may be NULL. */
+int pcf_compact(int is_f32, const void* st_dev, const void* sv_dev, const void* sv2_dev,
+                int value_bytes, const int32_t* flag_dev, int64_t ntot, const int64_t* off_in_dev,
+                const int64_t* src_dev, int64_t nout, int64_t* pos_dev, void* temp_dev,
+                int64_t temp_bytes, void* t_out_dev, void* v_out_dev, void* v2_out_dev,
+                int64_t* off_out_dev, void* stream);
+/* mean finalisation: v * T(scale[seg]) (core.scale) + keep-where-changed flags. */
+int pcf_scale_flag(int is_f32, const void* v_dev, const int64_t* off_dev, int64_t nseg,
+                   const double* scale_dev, int64_t ntot, void* sv_dev, int32_t* flag_dev,
+                   int32_t* status_dev, void* stream);
+/* variance / std finalisation from M2: T(M2 * scale[seg]) [then T(sqrt(.))] + flags. */
+int pcf_std_flag(int is_f32, int take_sqrt, const double* m2_dev, const int64_t* off_dev,
+                 int64_t nseg, const double* scale_dev, int64_t ntot, void* sv_dev,
+                 int32_t* flag_dev, int32_t* status_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,20 @@ SIGNATURES = {
         [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_dbl, c_int, c_int, c_dbl, c_dbl, c_vp,
          c_i64, c_i64p, c_i64p],
     ),
+    "pcf_probe_fp64": (c_int, [c_vp, c_int, c_int, c_vp]),
+    "pcf_scan_workspace": (c_int, [c_i64, c_i64p]),
+    "pcf_level_merge": (
+        c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
+                c_vp]),
+    "pcf_level_moments": (
+        c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
+                c_vp, c_vp]),
+    "pcf_compact": (
+        c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64,
+                c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pcf_scale_flag": (c_int, [c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "pcf_std_flag": (c_int, [c_int, c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
+                             c_vp]),
 }
 
 _lock = threading.Lock()

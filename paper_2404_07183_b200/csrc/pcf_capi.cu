@@ -376,3 +376,28 @@ done:
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ FP64 peak probe
+// Measures the dense FP64 FMA rate of this GPU (DFMA, 8 independent chains per thread,
+// full occupancy).  bench.py uses it as the roofline denominator for the pairwise
+// kernels, whose work is FP64-pipe / issue bound (no FP64 figure in MEASURED_PEAKS.json).
+namespace pcfb {
+__global__ void k_probe_dfma(double* out, int iters, double seed) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4,
+         a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) out[0] = s;  // keep the work alive
+}
+}  // namespace pcfb
+
+extern "C" int pcf_probe_fp64(double* out_dev, int iters, int blocks_per_sm, void* stream) {
+  const int nsm = num_sms_current();
+  pcfb::k_probe_dfma<<<nsm * blocks_per_sm, 256, 0, (cudaStream_t)stream>>>(out_dev, iters, 1.0);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_probe_fp64");
+}

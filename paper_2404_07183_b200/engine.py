@@ -140,3 +140,52 @@ def coll_inv_host(coll):
     inv = np.empty(coll.M, dtype=np.int64)
     inv[coll.perm_host] = np.arange(coll.M, dtype=np.int64)
     return inv
+
+
+def partition_items(host_items, n_smem, world, rank):
+    """Static cost-balanced split of the work queue over `world` GPUs.
+
+    Items are cost-sorted (LPT order) within the shared-memory and global groups; each
+    group is dealt out in snake order (0..W-1, W-1..0, ...), which keeps every rank's
+    share cost-sorted and balanced to within one item.  Every pair is owned by exactly
+    one rank, so results are identical for any world size.  Returns
+    (items_host_subset, n_smem_subset)."""
+    if world <= 1:
+        return host_items, n_smem
+    out, counts = [], []
+    for lo, hi in ((0, n_smem), (n_smem, host_items.shape[0])):
+        idx = np.arange(lo, hi)
+        k = idx - lo
+        cyc = k % (2 * world)
+        owner = np.where(cyc < world, cyc, 2 * world - 1 - cyc)
+        sel = host_items[idx[owner == rank]]
+        out.append(sel)
+        counts.append(sel.shape[0])
+    return np.concatenate(out, axis=0), counts[0]
+
+
+def items_to_device(host_items, device):
+    torch = _torch()
+    flat = np.ascontiguousarray(host_items, dtype=np.int32).reshape(-1)
+    if flat.size == 0:
+        flat = np.zeros(8, dtype=np.int32)
+    return torch.from_numpy(flat).to(device)
+
+
+def item_cells(host_items, sizes_sorted):
+    """Exact cell count of the pairs covered by the items: a pair (r, c) has
+    (n_r - 1) + (n_c - 1) finite steps plus the tail cell = n_r + n_c - 1 cells."""
+    if host_items.shape[0] == 0:
+        return 0
+    sizes = np.asarray(sizes_sorted, dtype=np.int64)
+    S = np.concatenate([[0], np.cumsum(sizes)])
+    it = np.asarray(host_items, dtype=np.int64)
+    rmax = int(it[:, 1].max())
+    r = it[:, 0:1] + np.arange(rmax)[None, :]
+    valid = np.arange(rmax)[None, :] < it[:, 1:2]
+    r = np.where(valid, r, 0)
+    c0 = np.maximum(it[:, 2:3], r + 1)
+    c1 = it[:, 3:4]
+    ncol = np.where(valid & (c1 > c0), c1 - c0, 0)
+    colsum = np.where(ncol > 0, S[c1.repeat(rmax, 1)] - S[np.minimum(c0, c1)], 0)
+    return int((ncol * (sizes[r] - 1) + colsum).sum())
