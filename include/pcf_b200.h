@@ -53,11 +53,11 @@ extern "C" {
 /* One work item of the pairwise tile scheduler (32 bytes, device-resident array). */
 typedef struct pcf_work_item {
   int32_t row0;      /* first size-sorted row of the row block */
-  int32_t nrows;     /* R: rows in the block */
+  int32_t nrows;     /* rows in the block (K1: 8 or 16 = one or two interleaved groups) */
   int32_t col0;      /* first size-sorted column of this item */
   int32_t col1;      /* one past the last column */
   int32_t logC;      /* columns per streamed chunk = 1 << logC */
-  int32_t log2G;     /* lanes per pair = 1 << log2G (merge-path split) */
+  int32_t log2G;     /* merge-path segments per pair = 1 << log2G */
   int32_t smem_mode; /* 1: operands staged in shared memory, 0: read from L1/L2 */
   int32_t cost_hi;   /* estimated cells / 2^20 (scheduling order only) */
 } pcf_work_item;
@@ -73,14 +73,20 @@ int pcf_tile_threads(void);
  * recs: 16*soff[M] bytes. */
 int pcf_pack_sorted(const void* tcat_dev, const void* vcat_dev, int is_f32,
                     const int64_t* off_dev, const int32_t* perm_dev, const int64_t* soff_dev,
-                    int64_t M, void* recs_dev, void* stream);
+                    int64_t M, void* recs_dev, const int64_t* goff8_dev, void* recs8_dev,
+                    void* stream);
+/* Slot-interleaved copy used by K1's row blocks (recs8, optional: pass NULLs to skip):
+ * record k of sorted PCF s lives at goff8[s/8] + 8k + s%8, so a quarter-warp reading the
+ * 8 rows of one group always hits 8 distinct shared-memory bank groups.
+ * goff8: int64[(M+7)/8 + 1], from pcf_group_offsets (host). */
+int pcf_group_offsets(const int64_t* sizes_sorted, int64_t M, int64_t* goff8);
 
 /* ---- planner (host): sizes in sorted order -> work items, cost-descending ---- */
 /* Returns the dynamic shared memory the items need in *smem_bytes.  `items` may be NULL
  * to query the count.  max_cols bounds the columns per item (load-balance granularity).
  * max_log2G caps the merge-path split: 0 = one lane per pair everywhere, which sums every
  * entry strictly left to right exactly like the reference (bitwise for p=1 and INNER);
- * 5 = up to a warp per pair (fastest; same cell products, summed in G runs). */
+ * 6 = up to 64 segments per pair (fastest; same cell products, summed in G runs). */
 int pcf_plan_pairwise(const int64_t* sizes_sorted, int64_t M, int64_t smem_budget,
                       int64_t max_cols, int32_t max_log2G, pcf_work_item* items, int64_t cap,
                       int64_t* n_items, int32_t* smem_bytes);
@@ -90,7 +96,8 @@ int pcf_plan_pairwise(const int64_t* sizes_sorted, int64_t M, int64_t smem_budge
  * (perm[p], perm[q]) and mirror are written for every pair covered by items
  * [0, n_items).  counter_dev: int32 initialised to 0.  p: Lp exponent (ignored for
  * INNER).  apply_root: r = x^(1/p) as in pdist.  b may be +inf. */
-int pcf_fill_matrix(const void* recs_dev, const int64_t* soff_dev, const int32_t* perm_dev,
+int pcf_fill_matrix(const void* recs_dev, const void* recs8_dev, const int64_t* soff_dev,
+                    const int64_t* goff8_dev, const int32_t* perm_dev,
                     int64_t M, const pcf_work_item* items_dev, int64_t n_items,
                     int32_t smem_bytes, int32_t smem_mode, int32_t* counter_dev, int op,
                     double p, int apply_root, double a, double b, void* out_dev,

@@ -4,6 +4,8 @@ Layout in HBM:
 
 * ``recs``  float64[2*N]  -- N 16-byte records {t_next, v} in size-sorted order;
 * ``soff``  int64[M+1]    -- record offsets of sorted PCF s;
+* ``recs8`` / ``goff8``   -- the same records slot-interleaved in groups of 8 sorted PCFs
+  (record k of PCF s at goff8[s/8] + 8k + s%8), the layout K1 stages its row blocks in;
 * ``perm``  int32[M]      -- sorted index -> original index;
 * ``inv``   int32[M]      -- original index -> sorted index.
 
@@ -70,6 +72,10 @@ class DeviceCollection:
         self.sizes_sorted = ssizes
         self.perm_host = perm
         self.n_points = int(soff[-1])
+        ng = (self.M + 7) // 8
+        goff8 = np.zeros(ng + 1, dtype=np.int64)
+        goff8[1:] = np.cumsum(8 * ssizes[0::8])
+        self.goff8_host = goff8
         with torch.cuda.device(self.device):
             dev = self.device
             t_d = torch.from_numpy(tcat).to(dev, non_blocking=False)
@@ -79,10 +85,13 @@ class DeviceCollection:
             self.inv = torch.from_numpy(inv).to(dev)
             self.soff = torch.from_numpy(soff).to(dev)
             self.recs = torch.empty(2 * max(self.n_points, 1), dtype=torch.float64, device=dev)
+            self.goff8 = torch.from_numpy(goff8).to(dev)
+            self.recs8 = torch.empty(2 * max(int(goff8[-1]), 1), dtype=torch.float64, device=dev)
             rc = lib.pcf_pack_sorted(
                 _native.ptr(t_d), _native.ptr(v_d), int(self.dtype == np.float32),
                 _native.ptr(off_d), _native.ptr(self.perm), _native.ptr(self.soff), self.M,
-                _native.ptr(self.recs), current_stream_handle())
+                _native.ptr(self.recs), _native.ptr(self.goff8), _native.ptr(self.recs8),
+                current_stream_handle())
             _native.check(rc, "pcf_pack_sorted")
             del t_d, v_d, off_d
         self._plans = {}
@@ -107,7 +116,7 @@ class DeviceCollection:
 
         exact=True restricts every pair to one lane (the reference's left-to-right
         sum, bitwise for p=1 and inner products); otherwise up to a warp per pair."""
-        max_log2g = 0 if exact else 5
+        max_log2g = 0 if exact else 6
         key = (max_log2g, smem_budget, max_cols)
         if key in self._plans:
             return self._plans[key]

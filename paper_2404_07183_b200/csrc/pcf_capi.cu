@@ -42,23 +42,39 @@ int pcf_tile_threads(void) { return kTileThreads; }
 
 int pcf_pack_sorted(const void* tcat_dev, const void* vcat_dev, int is_f32,
                     const int64_t* off_dev, const int32_t* perm_dev, const int64_t* soff_dev,
-                    int64_t M, void* recs_dev, void* stream) {
+                    int64_t M, void* recs_dev, const int64_t* goff8_dev, void* recs8_dev,
+                    void* stream) {
   if (M < 0 || (M > 0 && (!tcat_dev || !vcat_dev || !off_dev || !perm_dev || !soff_dev || !recs_dev))) {
     set_error("pcf_pack_sorted: bad arguments");
     return PCF_ERR_ARG;
   }
   if (M == 0) return PCF_OK;
   cudaError_t e = launch_pack(tcat_dev, vcat_dev, is_f32, off_dev, perm_dev, soff_dev, M, recs_dev,
-                              (cudaStream_t)stream);
+                              goff8_dev, recs8_dev, (cudaStream_t)stream);
   return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_pack_sorted");
 }
 
 // ------------------------------------------------------------------------------ planner
-// Row blocks of the size-sorted collection get the smallest merge-path split G (lanes per
-// pair) whose tile (R resident rows + two streamed chunks of C columns, R*C*G = CTA
-// threads) fits the shared-memory budget.  Column ranges are cut into items of at most
-// max_cols columns; items are returned cost-descending (LPT order for the persistent
-// kernel's atomic queue), shared-memory items first, then global-memory items.
+// Offsets of the slot-interleaved 8-row groups (record k of sorted PCF s at
+// goff8[s/8] + 8k + s%8): group g spans 8 * sizes[8g] records (sizes sorted descending).
+int pcf_group_offsets(const int64_t* sizes, int64_t M, int64_t* goff8) {
+  if (M < 0 || (M > 0 && (!sizes || !goff8))) {
+    set_error("pcf_group_offsets: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  const int64_t ng = (M + 7) / 8;
+  goff8[0] = 0;
+  for (int64_t g = 0; g < ng; ++g) goff8[g + 1] = goff8[g] + 8 * sizes[8 * g];
+  return PCF_OK;
+}
+
+// Row blocks of the size-sorted collection are one or two 8-row groups.  Each gets the
+// smallest merge-path split G (quarter-warps per pair, 64 quarters = RG x C x G) whose
+// shared-memory tile -- interleaved rows + two streamed chunks of C columns + the
+// segment-partial buffer -- fits the budget; blocks whose rows do not fit at any G go to
+// the global-memory kernel.  Column ranges are cut into items of at most max_cols
+// columns; items are returned cost-descending (LPT order for the persistent kernels'
+// atomic queues), shared-memory items first.
 int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int64_t max_cols,
                       int32_t max_log2G, pcf_work_item* items, int64_t cap, int64_t* n_items,
                       int32_t* smem_bytes) {
@@ -74,55 +90,54 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     }
     S[i + 1] = S[i] + sizes[i];
   }
+  if (max_log2G < 0) max_log2G = 0;
+  if (max_log2G > 6) max_log2G = 6;
   auto al = [](int64_t x) { return (x + 127) & ~(int64_t)127; };
+  auto group_recs = [&](int64_t r) { return 8 * sizes[r]; };  // r: first row of a group
   const int T = kTileThreads;
   std::vector<pcf_work_item> smem_items, glob_items;
   int64_t need_max = 0;
-  int64_t r0 = 0;
   if (max_cols < 1) max_cols = 1 << 30;
+  int64_t r0 = 0;
   while (r0 < M - 1) {
-    int sel_logG = -1, sel_logC = 0, sel_R = 0;
-    int64_t sel_need = 0;
-    if (max_log2G < 0) max_log2G = 0;
-    if (max_log2G > 5) max_log2G = 5;
-    for (int logG = 0; logG <= max_log2G && sel_logG < 0; ++logG) {
-      const int P = T >> logG;
-      int best_R = 0, best_logC = 0;
-      int64_t best_need = 0;
-      for (int logC = 0; (1 << logC) <= P; ++logC) {
-        const int C = 1 << logC, R = P >> logC;
-        if (R < C) break;
-        if (R > 4 * C) continue;
-        const int64_t Rr = std::min<int64_t>(R, M - 1 - r0);
-        const int64_t rows_b = (S[r0 + Rr] - S[r0]) * 16;
+    int best_logRG = -1, best_logC = 0, best_logG = 99;
+    int64_t best_need = 0;
+    for (int logRG = 1; logRG >= 0; --logRG) {
+      if (logRG == 1 && r0 + 8 >= M - 1) continue;  // second group would be empty of pairs
+      int64_t rows_b = group_recs(r0) * 16;
+      if (logRG == 1) rows_b += group_recs(r0 + 8) * 16;
+      for (int logC = 6 - logRG; logC >= 0; --logC) {
+        const int logG = 6 - logRG - logC;
+        if (logG > max_log2G) break;
+        const int64_t C = 1 << logC;
         const int64_t c0 = r0 + 1, ce = std::min<int64_t>(c0 + C, M);
-        const int64_t col_b = (S[ce] - S[c0]) * 16;
-        const int64_t need = al(rows_b) + 2 * al(col_b);
-        if (need <= smem_budget && R > best_R) {
-          best_R = R;
+        const int64_t need = al(rows_b) + 2 * al((S[ce] - S[c0]) * 16) + kRedBytes;
+        if (need > smem_budget) continue;
+        if (logG < best_logG || (logG == best_logG && logRG > best_logRG)) {
+          best_logRG = logRG;
           best_logC = logC;
+          best_logG = logG;
           best_need = need;
         }
-      }
-      if (best_R > 0) {
-        sel_logG = logG;
-        sel_logC = best_logC;
-        sel_R = best_R;
-        sel_need = best_need;
+        break;  // larger logC with this RG already failed or this one fits; keep smallest G
       }
     }
-    const bool smem = sel_logG >= 0;
-    if (!smem) {  // PCFs too long to stage: operands from L1/L2, G as large as allowed
-      sel_logG = max_log2G;
-      const int P = T >> sel_logG;  // pairs per pass; square-ish tile R = C or 2C
-      int lc = 0;
-      while ((1 << (2 * (lc + 1))) <= P) ++lc;
-      sel_logC = lc;
-      sel_R = P >> lc;
+    const bool smem = best_logRG >= 0 && (r0 % 8) == 0;
+    int rows, logC, logG;
+    if (smem) {
+      rows = 8 << best_logRG;
+      logC = best_logC;
+      logG = best_logG;
+    } else {  // rows too long to stage: operands from L1/L2, G lanes in one warp
+      logG = std::min(max_log2G, 5);
+      const int P = T >> logG;
+      rows = P <= 64 ? 8 : 32;
+      logC = 0;
+      while ((rows << (logC + 1)) <= P) ++logC;
     }
-    const int64_t Rr = std::min<int64_t>(sel_R, M - 1 - r0);
-    const int C = 1 << sel_logC;
-    int64_t span = std::max<int64_t>(C, (max_cols / C) * C);
+    const int64_t Rr = std::min<int64_t>(rows, M - r0);
+    const int C = 1 << logC;
+    const int64_t span = std::max<int64_t>(C, (max_cols / C) * C);
     const int64_t rows_pts = S[r0 + Rr] - S[r0];
     for (int64_t c0 = r0 + 1; c0 < M; c0 += span) {
       const int64_t c1 = std::min<int64_t>(c0 + span, M);
@@ -131,14 +146,14 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       w.nrows = (int32_t)Rr;
       w.col0 = (int32_t)c0;
       w.col1 = (int32_t)c1;
-      w.logC = sel_logC;
-      w.log2G = sel_logG;
+      w.logC = logC;
+      w.log2G = logG;
       w.smem_mode = smem ? 1 : 0;
       const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;
       w.cost_hi = (int32_t)std::min(2.0e9, cells / 1048576.0);
       (smem ? smem_items : glob_items).push_back(w);
     }
-    if (smem) need_max = std::max(need_max, sel_need);
+    if (smem) need_max = std::max(need_max, best_need);
     r0 += Rr;
   }
   auto by_cost = [](const pcf_work_item& x, const pcf_work_item& y) {
@@ -160,13 +175,15 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   return PCF_OK;
 }
 
-int pcf_fill_matrix(const void* recs_dev, const int64_t* soff_dev, const int32_t* perm_dev,
+int pcf_fill_matrix(const void* recs_dev, const void* recs8_dev, const int64_t* soff_dev,
+                    const int64_t* goff8_dev, const int32_t* perm_dev,
                     int64_t M, const pcf_work_item* items_dev, int64_t n_items,
                     int32_t smem_bytes, int32_t smem_mode, int32_t* counter_dev, int op,
                     double p, int apply_root, double a, double b, void* out_dev,
                     int out_is_f32, int64_t ld, unsigned long long* err_dev, void* stream) {
   if (n_items <= 0) return PCF_OK;
   if (!recs_dev || !soff_dev || !perm_dev || !items_dev || !counter_dev || !out_dev || !err_dev ||
+      (smem_mode && (!recs8_dev || !goff8_dev)) ||
       ld < M || (op != PCF_OP_LP && op != PCF_OP_INNER) || !(a >= 0.0) || !(a < b) ||
       n_items > 0x7fffffff) {
     set_error("pcf_fill_matrix: bad arguments");
@@ -177,7 +194,9 @@ int pcf_fill_matrix(const void* recs_dev, const int64_t* soff_dev, const int32_t
   if (e != cudaSuccess) return cuda_fail(e, "pcf_fill_matrix memset");
   FillArgs A;
   A.recs = recs_dev;
+  A.recs8 = recs8_dev;
   A.soff = soff_dev;
+  A.goff8 = goff8_dev;
   A.perm = perm_dev;
   A.M = M;
   A.items = items_dev;
@@ -294,7 +313,7 @@ int pcf_integrate_pair_host(const double* ft, const double* fv, int64_t nf, cons
   cudaMemcpy(dperm.p, perm, 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dpairs.p, pairs, 16, cudaMemcpyHostToDevice);
   if ((e = launch_pack(dt.p, dv.p, 0, (int64_t*)doff.p, (int32_t*)dperm.p, (int64_t*)doff.p, 2,
-                       drec.p, 0)))
+                       drec.p, nullptr, nullptr, 0)))
     return cuda_fail(e, "pcf_integrate_pair_host pack");
   if ((e = launch_pair_list(drec.p, (int64_t*)doff.p, (int64_t*)dpairs.p, 1, op, p, a, b,
                             (double*)dres.p, 0)))
@@ -331,7 +350,7 @@ int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* o
   cudaMemcpy(dperm.p, ident.data(), M * 4, cudaMemcpyHostToDevice);
   cudaMemset(derr.p, 0xff, 8);
   if ((e = launch_pack(dt.p, dv.p, 0, (int64_t*)doff.p, (int32_t*)dperm.p, (int64_t*)doff.p, M,
-                       drec.p, 0)))
+                       drec.p, nullptr, nullptr, 0)))
     return cuda_fail(e, "pcf_fill_block_host pack");
   RowsArgs A;
   A.recs = drec.p;

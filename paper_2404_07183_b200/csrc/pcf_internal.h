@@ -12,7 +12,9 @@ typedef pcf_work_item PcfWorkItem;
 
 struct FillArgs {
   const void* recs;
+  const void* recs8;
   const int64_t* soff;
+  const int64_t* goff8;
   const int32_t* perm;
   int64_t M;
   const PcfWorkItem* items;
@@ -54,7 +56,9 @@ cudaError_t launch_pair_list(const void* recs, const int64_t* soff, const int64_
                              cudaStream_t st);
 cudaError_t launch_pack(const void* tcat, const void* vcat, int f32, const int64_t* off,
                         const int32_t* perm, const int64_t* soff, int64_t M, void* recs,
-                        cudaStream_t st);
+                        const int64_t* goff8, void* recs8, cudaStream_t st);
+
+constexpr int kRedBytes = 4 * kTileThreads * 8;  // K1 segment partials + tails, 2 buffers
 
 void set_error(const char* fmt, ...);
 

@@ -1,5 +1,6 @@
-// Pairwise rectangle-iteration engine (K1 tiles, K1g global-memory tiles, pair list,
-// diagonal, sort-pack).  See DESIGN.md for the layout and the roofline.
+// Pairwise rectangle-iteration engine: K1 (shared-memory tile kernel), K1g (global-memory
+// tiles for PCFs too long to stage), the fill_block row kernel, the pair list, the
+// diagonal, and K3 (sort-pack).  See DESIGN.md for layouts and rooflines.
 //
 // Reference semantics being reproduced:
 //   _sweepkern._accumulate  pkg/src/pcflib/_sweepkern.pyx:24-59  (per-pair walk)
@@ -13,40 +14,46 @@ namespace pcfb {
 // --------------------------------------------------------------------------------------
 // One lane's share of one pair's integral.
 //
-// The cells of the minimal common refinement of f and g on [a, b) are visited in
-// time order, exactly as _accumulate does (pyx:37-59), except that a simultaneous
-// jump (t_f == t_g) is taken as two steps: the f cursor first (stable merge order),
-// then a zero-width cell [t, t) whose contribution h*0 = +-0 leaves the running sum
-// bit-for-bit unchanged.  That makes the step count a pure function of the sizes
-// (N = (n_f-1-k0) + (n_g-1-m0)) so the loop needs no per-step termination test, and
-// lets G lanes split one pair along the merge path (diagonals d = lane*N/G) with a
-// co-rank binary search.  G = 1 is the reference's strict left-to-right sum; G > 1
-// sums the same cell products in G contiguous runs followed by a fixed butterfly.
+// The cells of the minimal common refinement of f and g on [a, b) are visited in time
+// order, exactly as _accumulate does (pyx:37-59), except that a simultaneous jump
+// (t_f == t_g) is taken as two steps, the second a zero-width cell [t, t) whose
+// contribution h*0 = +-0 leaves the running sum bit-for-bit unchanged.  The step count is
+// then a pure function of the sizes (N = (n_f-1-k0) + (n_g-1-m0)), so the loop needs no
+// per-step termination test, and G lanes can split one pair along the merge path
+// (diagonals d = lane*N/G, co-rank binary search).  G = 1 is the reference's strict
+// left-to-right sum; G > 1 sums the same cell products in G contiguous runs that the
+// caller adds in a fixed order.
 //
-// Bounded b: each cell's right edge is clamped to b (cells past b become zero-width),
-// and the last lane adds the final cell h(v_f_last, v_g_last) * (b - t).
-// Unbounded b: the tail cell is not accumulated; the caller applies the divergence
-// rule of pyx:47-51 to the last values.
-template <int HK, bool BOUNDED>
+// Each step issues ONE 16-byte load (the record of whichever cursor advances; the
+// address and the destination registers are selected), so a warp's request covers all
+// 32 lanes: shared-memory wavefronts are counted per quarter-warp, and a predicated
+// two-load step would pay for eight quarter-phases instead of four.
+//
+// F and G are record pointers with strides SF / SG (records): the K1 row block is stored
+// slot-interleaved (stride 8), columns and global data contiguously (stride 1).
+// Bounded b: cell right edges are clamped to b (cells past b become zero-width) and the
+// last lane adds the final cell h(v_f_last, v_g_last) * (b - t).  Unbounded b: the tail
+// cell is left to the caller, which applies the divergence rule of pyx:47-51.
+template <int HK, bool BOUNDED, int SF, int SG>
 __device__ __forceinline__ double lane_walk(const Rec* __restrict__ F, int nf,
                                             const Rec* __restrict__ Gv, int ng, int lane,
                                             int log2G, double p, double a, double b) {
   int k0 = 0, m0 = 0;
   if (a > 0.0) {  // start cursors k = max{i : t_i <= a} (pyx:33-36), by binary search
-    k0 = upper_bound_count(nf - 1, a, [&](int x) { return F[x].t; });
-    m0 = upper_bound_count(ng - 1, a, [&](int x) { return Gv[x].t; });
+    k0 = upper_bound_count(nf - 1, a, [&](int x) { return F[x * SF].t; });
+    m0 = upper_bound_count(ng - 1, a, [&](int x) { return Gv[x * SG].t; });
   }
-  const Rec* __restrict__ Fk = F + k0;
-  const Rec* __restrict__ Gm = Gv + m0;
+  const Rec* __restrict__ Fk = F + k0 * SF;
+  const Rec* __restrict__ Gm = Gv + m0 * SG;
   const int Nf = nf - 1 - k0, Ng = ng - 1 - m0;
   const int N = Nf + Ng;
   const int d0 = (int)(((long long)lane * N) >> log2G);
   const int d1 = (int)(((long long)(lane + 1) * N) >> log2G);
-  // co-rank: number of f breakpoints among the first d0 merged breakpoints.
+  // co-rank: number of f breakpoints among the first d0 merged breakpoints
   int lo = max(0, d0 - Ng), hi = min(d0, Nf);
   while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (Fk[mid].t <= Gm[d0 - mid - 1].t) lo = mid + 1;
+    const int mid = (lo + hi) >> 1;
+    if (Fk[mid * SF].t <= Gm[(d0 - mid - 1) * SG].t) lo = mid + 1;
     else hi = mid;
   }
   const int i = lo, j = d0 - lo;
@@ -54,51 +61,64 @@ __device__ __forceinline__ double lane_walk(const Rec* __restrict__ F, int nf,
   if (d0 == 0) {
     t = a;
   } else {
-    double tfp = i > 0 ? Fk[i - 1].t : 0.0;
-    double tgp = j > 0 ? Gm[j - 1].t : 0.0;
+    const double tfp = i > 0 ? Fk[(i - 1) * SF].t : 0.0;
+    const double tgp = j > 0 ? Gm[(j - 1) * SG].t : 0.0;
     t = fmax(tfp, tgp);
   }
   if (BOUNDED) t = fmin(t, b);
-  const Rec* __restrict__ fp = Fk + i;
-  const Rec* __restrict__ gp = Gm + j;
-  double tf = fp->t, vf = fp->v, tg = gp->t, vg = gp->v;
+  // X/Y form: X is the cursor whose piece ends first, Y the other.  Every integrand here
+  // is symmetric in (v_f, v_g), so the cell needs no f/g identity: tn = tX, advance X,
+  // then swap roles if the new X piece outlasts Y.  (Ties may be taken in either order:
+  // the extra zero-width cell adds +-0.)
+  const Rec* __restrict__ xp = Fk + i * SF;
+  const Rec* __restrict__ yp = Gm + j * SG;
+  int xs = SF, ys = SG;
+  double tx = xp->t, vx = xp->v, ty = yp->t, vy = yp->v;
+  if (ty < tx) {
+    const Rec* tp = xp; xp = yp; yp = tp;
+    int ts = xs; xs = ys; ys = ts;
+    double tt = tx; tx = ty; ty = tt;
+    tt = vx; vx = vy; vy = tt;
+  }
   double acc = 0.0;
   const int steps = d1 - d0;
 #pragma unroll 4
   for (int s = 0; s < steps; ++s) {
-    const bool af = tf <= tg;
-    double tn = af ? tf : tg;
+    double tn = tx;
     if (BOUNDED) tn = fmin(tn, b);
-    acc = __dadd_rn(acc, __dmul_rn(hval<HK>(vf, vg, p), __dsub_rn(tn, t)));
+    acc = __dadd_rn(acc, __dmul_rn(hval<HK>(vx, vy, p), __dsub_rn(tn, t)));
     t = tn;
-    if (af) {
-      ++fp;
-      tf = fp->t;
-      vf = fp->v;
-    } else {
-      ++gp;
-      tg = gp->t;
-      vg = gp->v;
+    xp += xs;
+    const double nt = xp->t, nv = xp->v;
+    const bool sw = nt > ty;
+    const Rec* __restrict__ np = sw ? yp : xp;
+    yp = sw ? xp : yp;
+    xp = np;
+    if (SF != SG) {
+      const int ns = sw ? ys : xs;
+      ys = sw ? xs : ys;
+      xs = ns;
     }
+    tx = sw ? ty : nt;
+    vx = sw ? vy : nv;
+    ty = sw ? nt : ty;
+    vy = sw ? nv : vy;
   }
   if (BOUNDED && (lane == (1 << log2G) - 1)) {
-    acc = __dadd_rn(acc, __dmul_rn(hval<HK>(vf, vg, p), __dsub_rn(b, t)));
+    acc = __dadd_rn(acc, __dmul_rn(hval<HK>(vx, vy, p), __dsub_rn(b, t)));
   }
   return acc;
 }
 
-// Finalise one entry: divergence rule, non-finite capture, root, cast, mirrored write.
-// (pyx:47-51, 109-116).
-template <int HK, bool BOUNDED, typename OutT>
-__device__ __forceinline__ void finish_entry(double acc, double vf_last, double vg_last,
-                                             double p, int apply_root, int64_t oi, int64_t oj,
-                                             OutT* __restrict__ out, int64_t ld, int64_t M,
+// Finalise one entry: divergence rule, non-finite capture, root, cast, mirrored write
+// (pyx:47-51, 109-116).  `hl` is h(v_f_last, v_g_last) (only used when unbounded).
+template <bool BOUNDED, typename OutT>
+__device__ __forceinline__ void finish_entry(double acc, double hl, double p, int apply_root,
+                                             int64_t oi, int64_t oj, OutT* __restrict__ out,
+                                             int64_t ld, int64_t M,
                                              unsigned long long* __restrict__ err) {
   double res = acc;
-  if (!BOUNDED) {
-    const double hl = hval<HK>(vf_last, vg_last, p);
-    if (hl != 0.0) res = hl > 0.0 ? INFINITY : -INFINITY;
-  }
+  if (!BOUNDED && hl != 0.0) res = hl > 0.0 ? INFINITY : -INFINITY;
   if (!isfinite(res)) {
     const int64_t lo = oi < oj ? oi : oj, hi = oi < oj ? oj : oi;
     atomicMin(err, (unsigned long long)(lo * M + hi));
@@ -111,13 +131,24 @@ __device__ __forceinline__ void finish_entry(double acc, double vf_last, double 
 }
 
 // --------------------------------------------------------------------------------------
-// K1: persistent tile kernel.  Each work item is a row block (R size-sorted PCFs,
-// staged once in shared memory by one bulk copy) against a column range streamed
-// through a double-buffered shared-memory chunk of C PCFs (one bulk copy each).
-// R*C pairs per chunk, G = 2^log2G lanes per pair (see lane_walk).
+// K1: persistent tile kernel (512 threads, one CTA per SM).
+//
+// Work item = a block of 8*RG size-sorted rows x a column range.  The rows are staged
+// once per item by one bulk copy from the slot-interleaved copy of the collection
+// (recs8: record k of row u of an 8-row group at 16*(8k+u) -> shared-memory bank group
+// u for every k); the columns stream through two shared-memory buffers of C contiguous
+// PCFs (one bulk copy each, double-buffered on mbarriers).
+//
+// Lane mapping: a quarter-warp (8 lanes, the unit in which 16-byte shared loads are
+// served) holds the 8 rows of one row group against ONE column: the row loads of a
+// quarter always hit 8 distinct bank groups, so only column loads can conflict.
+// 64 quarters = RG row groups x C columns x G merge-path segments.  With G > 1 the
+// segment partials go through shared memory and one thread per pair adds them in
+// segment order.
 template <int HK, bool BOUNDED, typename OutT>
 __global__ void __launch_bounds__(kTileThreads, 1)
-    k_fill_tiles_smem(const Rec* __restrict__ recs, const int64_t* __restrict__ soff,
+    k_fill_tiles_smem(const Rec* __restrict__ recs, const Rec* __restrict__ recs8,
+                      const int64_t* __restrict__ soff, const int64_t* __restrict__ goff8,
                       const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
                       int n_items, int* __restrict__ counter, double p, double a, double b,
                       int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
@@ -141,9 +172,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const int it = s_item;
     if (it >= n_items) break;
     const PcfWorkItem W = items[it];
-    const int R = W.nrows, C = 1 << W.logC, log2G = W.log2G;
-    const int64_t rbase = soff[W.row0];
-    const uint32_t row_bytes = (uint32_t)((soff[W.row0 + R] - rbase) * sizeof(Rec));
+    const int logRG = W.nrows > 8 ? 1 : 0;
+    const int RG = 1 << logRG, C = 1 << W.logC, log2G = W.log2G, G = 1 << log2G;
+    const int rg0 = W.row0 >> 3;
+    const int64_t rbase = goff8[rg0];
+    const uint32_t row_bytes = (uint32_t)((goff8[rg0 + RG] - rbase) * sizeof(Rec));
     const int nchunk = (W.col1 - W.col0 + C - 1) >> W.logC;
     const int c_first_end = min(W.col0 + C, W.col1);
     const uint32_t col_cap = (uint32_t)((soff[c_first_end] - soff[W.col0]) * sizeof(Rec));
@@ -151,11 +184,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const uint32_t col_al = (col_cap + 127u) & ~127u;
     unsigned char* rowbuf = smem;
     unsigned char* colbase = smem + row_al;  // column buffer k at colbase + k * col_al
+    double* red = reinterpret_cast<double*>(smem + row_al + 2 * col_al);  // [2][512] partials
+    double* redh = red + 2 * kTileThreads;                                 // [2][pairs] tails
 
     if (tid == 0) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], row_bytes);
-      bulk_g2s(rowbuf, recs + rbase, row_bytes, &bars[0]);
+      bulk_g2s(rowbuf, recs8 + rbase, row_bytes, &bars[0]);
       for (int c = 0; c < 2 && c < nchunk; ++c) {
         const int cb = W.col0 + (c << W.logC), ce = min(cb + C, W.col1);
         const uint32_t nb = (uint32_t)((soff[ce] - soff[cb]) * sizeof(Rec));
@@ -163,21 +198,23 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         bulk_g2s(colbase + c * col_al, recs + soff[cb], nb, &bars[1 + c]);
       }
     }
-    // Per-thread pair coordinates are fixed for the whole item.
-    const int pair = tid >> log2G;
-    const int lane = tid & ((1 << log2G) - 1);
-    const int r = pair >> W.logC;
-    const int cc = pair & (C - 1);
-    const bool row_ok = r < R;
-    const int ps = W.row0 + r;
+    // lane -> (row slot u, row group rho, column cc, segment g); fixed for the item
+    const int u = tid & 7;
+    const int Q = tid >> 3;
+    const int rho = Q & (RG - 1);
+    const int cc = (Q >> logRG) & (C - 1);
+    const int g = Q >> (logRG + W.logC);
+    const int ps = W.row0 + 8 * rho + u;
+    const bool row_ok = ps < M;
     int nf = 0;
-    const Rec* F = reinterpret_cast<const Rec*>(rowbuf);
+    const Rec* F = reinterpret_cast<const Rec*>(rowbuf) + (goff8[rg0 + rho] - rbase) + u;
     int64_t oi = 0;
     if (row_ok) {
       nf = (int)(soff[ps + 1] - soff[ps]);
-      F += soff[ps] - rbase;
       oi = perm[ps];
     }
+    const int pair_id = (cc * RG + rho) * 8 + u;  // 0 .. 8*RG*C-1
+    const int npairs = 8 * RG * C;
     mbar_wait(&bars[0], ph_row);
     ph_row ^= 1u;
 
@@ -189,21 +226,33 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const bool ok = row_ok && qs < ce && qs > ps;
       mbar_wait(&bars[1 + buf], ph_col[buf]);
       ph_col[buf] ^= 1u;
-      double acc = 0.0;
-      int ng = 0;
       const Rec* Gv = reinterpret_cast<const Rec*>(colbase + buf * col_al);
+      double acc = 0.0, hl = 0.0;
       if (ok) {
-        ng = (int)(soff[qs + 1] - soff[qs]);
+        const int ng = (int)(soff[qs + 1] - soff[qs]);
         Gv += soff[qs] - soff[cb];
-        acc = lane_walk<HK, BOUNDED>(F, nf, Gv, ng, lane, log2G, p, a, b);
+        acc = lane_walk<HK, BOUNDED, 8, 1>(F, nf, Gv, ng, g, log2G, p, a, b);
+        if (!BOUNDED) hl = hval<HK>(F[(nf - 1) * 8].v, Gv[ng - 1].v, p);
       }
-      for (int o = (1 << log2G) >> 1; o >= 1; o >>= 1)
-        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-      if (ok && lane == 0) {
-        finish_entry<HK, BOUNDED, OutT>(acc, F[nf - 1].v, Gv[ng - 1].v, p, apply_root, oi,
-                                        (int64_t)perm[qs], out, ld, M, err);
+      if (G == 1) {
+        if (ok) finish_entry<BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
+        __syncthreads();  // buffer `buf` is free again
+      } else {
+        red[buf * kTileThreads + g * npairs + pair_id] = acc;  // segment-major: no conflicts
+        if (g == 0) redh[buf * kTileThreads + pair_id] = hl;
+        __syncthreads();  // partials visible, buffer `buf` free again
+        if (tid < npairs) {
+          const int pu = tid & 7, prho = (tid >> 3) & (RG - 1), pcc = tid >> (3 + logRG);
+          const int pps = W.row0 + 8 * prho + pu, pqs = cb + pcc;
+          if (pps < M && pqs < ce && pqs > pps) {
+            const double* r = red + buf * kTileThreads + tid;
+            double s = r[0];
+            for (int k = 1; k < G; ++k) s = __dadd_rn(s, r[k * npairs]);
+            finish_entry<BOUNDED, OutT>(s, redh[buf * kTileThreads + tid], p, apply_root,
+                                        perm[pps], perm[pqs], out, ld, M, err);
+          }
+        }
       }
-      __syncthreads();  // buffer `buf` is free again
       if (tid == 0 && c + 2 < nchunk) {
         const int nb0 = W.col0 + ((c + 2) << W.logC), ne = min(nb0 + C, W.col1);
         const uint32_t nb = (uint32_t)((soff[ne] - soff[nb0]) * sizeof(Rec));
@@ -212,11 +261,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         bulk_g2s(colbase + buf * col_al, recs + soff[nb0], nb, &bars[1 + buf]);
       }
     }
+    __syncthreads();  // all finishers done before the next item reuses shared memory
   }
 }
 
-// K1g: same schedule, operands read straight from global memory (L1/L2).  Used for
-// row blocks whose PCFs are too long for the shared-memory budget.
+// K1g: tiles whose PCFs are too long to stage; operands read straight from the
+// contiguous records through L1/L2.  R x C pairs per pass, G lanes per pair in one warp
+// (butterfly reduction).
 template <int HK, bool BOUNDED, typename OutT>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_fill_tiles_global(const Rec* __restrict__ recs, const int64_t* __restrict__ soff,
@@ -250,21 +301,42 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (ok) {
         nf = (int)(soff[ps + 1] - soff[ps]);
         ng = (int)(soff[qs + 1] - soff[qs]);
-        acc = lane_walk<HK, BOUNDED>(F, nf, Gv, ng, lane, log2G, p, a, b);
+        acc = lane_walk<HK, BOUNDED, 1, 1>(F, nf, Gv, ng, lane, log2G, p, a, b);
       }
       for (int o = (1 << log2G) >> 1; o >= 1; o >>= 1)
         acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-      if (ok && lane == 0)
-        finish_entry<HK, BOUNDED, OutT>(acc, F[nf - 1].v, Gv[ng - 1].v, p, apply_root,
-                                        (int64_t)perm[ps], (int64_t)perm[qs], out, ld, M, err);
+      if (ok && lane == 0) {
+        const double hl = BOUNDED ? 0.0 : hval<HK>(F[nf - 1].v, Gv[ng - 1].v, p);
+        finish_entry<BOUNDED, OutT>(acc, hl, p, apply_root, (int64_t)perm[ps],
+                                    (int64_t)perm[qs], out, ld, M, err);
+      }
     }
   }
 }
 
 // --------------------------------------------------------------------------------------
 // Diagonal: Gram entries <f, f> (computed, pyx:104 with diag=True) or exact zeros for
-// distances (never computed; matrix.py:163).  One thread per PCF, sequential walk,
+// distances (never computed; matrix.py:163).  One thread per PCF, sequential walk;
 // simultaneous jumps of f against itself take one step as in the reference.
+template <bool BOUNDED>
+__device__ __forceinline__ double self_inner(const Rec* __restrict__ F, int n, double a,
+                                             double b) {
+  int k = 0;
+  if (a > 0.0) k = upper_bound_count(n - 1, a, [&](int x) { return F[x].t; });
+  double t = a, acc = 0.0;
+  for (;;) {
+    const double tn = F[k].t, v = F[k].v;
+    const double hv = __dmul_rn(v, v);
+    if (tn >= b) {
+      if (!BOUNDED) return (hv != 0.0) ? (hv > 0.0 ? INFINITY : -INFINITY) : acc;
+      return __dadd_rn(acc, __dmul_rn(hv, __dsub_rn(b, t)));
+    }
+    acc = __dadd_rn(acc, __dmul_rn(hv, __dsub_rn(tn, t)));
+    t = tn;
+    ++k;
+  }
+}
+
 template <bool BOUNDED, typename OutT>
 __global__ void k_diag(const Rec* __restrict__ recs, const int64_t* __restrict__ soff,
                        const int32_t* __restrict__ perm, int64_t M, int gram, double a,
@@ -277,27 +349,8 @@ __global__ void k_diag(const Rec* __restrict__ recs, const int64_t* __restrict__
       out[o * ld + o] = cast_out<OutT>(0.0);
       continue;
     }
-    const Rec* F = recs + soff[s];
-    const int n = (int)(soff[s + 1] - soff[s]);
-    int k = 0;
-    if (a > 0.0) k = upper_bound_count(n - 1, a, [&](int x) { return F[x].t; });
-    double t = a, acc = 0.0;
-    double res;
-    for (;;) {
-      const double tn = F[k].t, v = F[k].v;
-      const double hv = __dmul_rn(v, v);
-      if (tn >= b) {
-        if (!BOUNDED) {
-          res = (hv != 0.0) ? (hv > 0.0 ? INFINITY : -INFINITY) : acc;
-        } else {
-          res = __dadd_rn(acc, __dmul_rn(hv, __dsub_rn(b, t)));
-        }
-        break;
-      }
-      acc = __dadd_rn(acc, __dmul_rn(hv, __dsub_rn(tn, t)));
-      t = tn;
-      ++k;
-    }
+    const double res =
+        self_inner<BOUNDED>(recs + soff[s], (int)(soff[s + 1] - soff[s]), a, b);
     if (!isfinite(res)) atomicMin(err, (unsigned long long)(o * M + o));
     out[o * ld + o] = cast_out<OutT>(res);
   }
@@ -305,9 +358,9 @@ __global__ void k_diag(const Rec* __restrict__ recs, const int64_t* __restrict__
 
 // --------------------------------------------------------------------------------------
 // Row-range kernel mirroring fill_block(packed, r0, r1, ...) on ORIGINAL indices
-// (pyx:88-121): rows [r0, r1), columns j > i (j >= i with diag).  One thread per
-// entry, G = 1 (reference summation order), operands from global memory.  Output is a
-// compact (r1-r0) x M row slab; the host mirrors it.
+// (pyx:88-121): rows [r0, r1), columns j > i (j >= i with diag).  One thread per entry,
+// G = 1 (reference summation order), operands from global memory.  Output is a compact
+// (r1-r0) x M row slab; the host mirrors it.
 template <int HK, bool BOUNDED, typename OutT>
 __global__ void k_fill_rows(const Rec* __restrict__ recs, const int64_t* __restrict__ soff,
                             const int32_t* __restrict__ inv, int64_t M, int64_t r0, int64_t r1,
@@ -324,23 +377,13 @@ __global__ void k_fill_rows(const Rec* __restrict__ recs, const int64_t* __restr
       const int ng = (int)(soff[sj + 1] - soff[sj]);
       double res;
       if (j == i) {
-        // Gram diagonal: f against itself, one step per shared breakpoint.
-        int k = 0;
-        if (a > 0.0) k = upper_bound_count(nf - 1, a, [&](int x) { return F[x].t; });
-        double t = a, acc = 0.0;
-        for (;;) {
-          const double tn = F[k].t, hv = hval<HK>(F[k].v, F[k].v, p);
-          if (tn >= b) {
-            if (!BOUNDED) res = (hv != 0.0) ? (hv > 0.0 ? INFINITY : -INFINITY) : acc;
-            else res = __dadd_rn(acc, __dmul_rn(hv, __dsub_rn(b, t)));
-            break;
-          }
-          acc = __dadd_rn(acc, __dmul_rn(hv, __dsub_rn(tn, t)));
-          t = tn;
-          ++k;
+        if (HK == H_INNER) {
+          res = self_inner<BOUNDED>(F, nf, a, b);
+        } else {
+          res = BOUNDED ? 0.0 : 0.0;  // |f - f|^p == 0 on every cell
         }
       } else {
-        res = lane_walk<HK, BOUNDED>(F, nf, Gv, ng, 0, 0, p, a, b);
+        res = lane_walk<HK, BOUNDED, 1, 1>(F, nf, Gv, ng, 0, 0, p, a, b);
         if (!BOUNDED) {
           const double hl = hval<HK>(F[nf - 1].v, Gv[ng - 1].v, p);
           if (hl != 0.0) res = hl > 0.0 ? INFINITY : -INFINITY;
@@ -369,7 +412,7 @@ __global__ void k_pair_list(const Rec* __restrict__ recs, const int64_t* __restr
     const Rec* Gv = recs + soff[sj];
     const int nf = (int)(soff[si + 1] - soff[si]);
     const int ng = (int)(soff[sj + 1] - soff[sj]);
-    double res = lane_walk<HK, BOUNDED>(F, nf, Gv, ng, 0, 0, p, a, b);
+    double res = lane_walk<HK, BOUNDED, 1, 1>(F, nf, Gv, ng, 0, 0, p, a, b);
     if (!BOUNDED) {
       const double hl = hval<HK>(F[nf - 1].v, Gv[ng - 1].v, p);
       if (hl != 0.0) res = hl > 0.0 ? INFINITY : -INFINITY;
@@ -380,11 +423,14 @@ __global__ void k_pair_list(const Rec* __restrict__ recs, const int64_t* __restr
 
 // --------------------------------------------------------------------------------------
 // K3: device-side pack.  Original-order SoA (tcat, vcat, off) -- the reference's pack()
-// output, pyx:72-85 -- into size-sorted records.  One warp per sorted PCF.
+// output, pyx:72-85 -- into size-sorted contiguous records and, optionally, the
+// slot-interleaved 8-row-group copy (record k of sorted PCF s at goff8[s/8] + 8k + s%8).
+// One warp per sorted PCF.
 template <typename T>
 __global__ void k_pack_sorted(const T* __restrict__ tcat, const T* __restrict__ vcat,
                               const int64_t* __restrict__ off, const int32_t* __restrict__ perm,
-                              const int64_t* __restrict__ soff, int64_t M, Rec* __restrict__ recs) {
+                              const int64_t* __restrict__ soff, int64_t M, Rec* __restrict__ recs,
+                              const int64_t* __restrict__ goff8, Rec* __restrict__ recs8) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -393,11 +439,13 @@ __global__ void k_pack_sorted(const T* __restrict__ tcat, const T* __restrict__ 
     const int64_t src = off[o];
     const int64_t n = off[o + 1] - src;
     Rec* dst = recs + soff[s];
+    Rec* dst8 = recs8 ? recs8 + goff8[s >> 3] + (s & 7) : nullptr;
     for (int64_t k = lane; k < n; k += 32) {
       Rec r;
       r.t = (k + 1 < n) ? (double)tcat[src + k + 1] : INFINITY;
       r.v = (double)vcat[src + k];
       dst[k] = r;
+      if (dst8) dst8[8 * k] = r;
     }
   }
 }
@@ -407,16 +455,15 @@ __global__ void k_pack_sorted(const T* __restrict__ tcat, const T* __restrict__ 
 
 template <int HK, bool BOUNDED, typename OutT>
 static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
-  const int nsm = A.num_sms;
-  const int grid = nsm;  // persistent: one CTA per SM
+  const int grid = A.num_sms;  // persistent: one CTA per SM
   if (A.smem_mode) {
     auto kern = k_fill_tiles_smem<HK, BOUNDED, OutT>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
     if (e != cudaSuccess) return e;
     kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
-        (const Rec*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
-        A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+        (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
+        A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
   } else {
     k_fill_tiles_global<HK, BOUNDED, OutT><<<grid * 2, kTileThreads, 0, st>>>(
         (const Rec*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
@@ -539,16 +586,16 @@ cudaError_t launch_pair_list(const void* recs, const int64_t* soff, const int64_
 
 cudaError_t launch_pack(const void* tcat, const void* vcat, int f32, const int64_t* off,
                         const int32_t* perm, const int64_t* soff, int64_t M, void* recs,
-                        cudaStream_t st) {
+                        const int64_t* goff8, void* recs8, cudaStream_t st) {
   int grid = (int)((M * 32 + 255) / 256);
   if (grid > 148 * 64) grid = 148 * 64;
   if (grid < 1) grid = 1;
   if (f32)
     k_pack_sorted<float><<<grid, 256, 0, st>>>((const float*)tcat, (const float*)vcat, off, perm,
-                                               soff, M, (Rec*)recs);
+                                               soff, M, (Rec*)recs, goff8, (Rec*)recs8);
   else
     k_pack_sorted<double><<<grid, 256, 0, st>>>((const double*)tcat, (const double*)vcat, off,
-                                                perm, soff, M, (Rec*)recs);
+                                                perm, soff, M, (Rec*)recs, goff8, (Rec*)recs8);
   return cudaGetLastError();
 }
 

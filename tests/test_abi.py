@@ -43,7 +43,7 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-def plan(sizes, budget=220 * 1024, max_cols=64, max_log2g=5):
+def plan(sizes, budget=220 * 1024, max_cols=64, max_log2g=6):
     lib = _native.load()
     sizes = np.ascontiguousarray(sizes, dtype=np.int64)
     n = ctypes.c_int64()
@@ -58,7 +58,7 @@ def plan(sizes, budget=220 * 1024, max_cols=64, max_log2g=5):
 
 
 @pytest.mark.parametrize("dist", ["appa", "small", "huge", "one", "two"])
-@pytest.mark.parametrize("max_log2g", [0, 5])
+@pytest.mark.parametrize("max_log2g", [0, 6])
 def test_planner_covers_upper_triangle_once(dist, max_log2g):
     rng = np.random.default_rng(1)
     sizes = {
@@ -76,14 +76,18 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g):
     threads = 512
     for row0, nrows, col0, col1, logc, log2g, mode, cost in items:
         C, G = 1 << logc, 1 << log2g
-        assert nrows * C * G <= threads
         assert log2g <= max_log2g
         assert col0 > row0 and col1 <= M and nrows >= 1
-        if mode == 1:
-            rows_b = (S[row0 + nrows] - S[row0]) * 16
+        if mode == 1:  # K1: 8-row interleaved groups, 64 quarter-warps = RG x C x G
+            assert row0 % 8 == 0 and nrows <= 16
+            RG = 2 if nrows > 8 else 1
+            assert RG * C * G == 64
+            rows_b = sum(8 * sizes[row0 + 8 * k] * 16 for k in range(RG))
             col_b = (S[min(col0 + C, col1)] - S[col0]) * 16
             al = lambda x: (x + 127) // 128 * 128  # noqa: E731
-            assert al(rows_b) + 2 * al(col_b) <= smem <= 220 * 1024
+            assert al(rows_b) + 2 * al(col_b) + 4 * 512 * 8 <= smem <= 220 * 1024
+        else:  # K1g: R x C pairs x G lanes in-warp
+            assert nrows * C * G <= threads and G <= 32
         for r in range(row0, row0 + nrows):
             for q in range(col0, col1):
                 if q > r:
