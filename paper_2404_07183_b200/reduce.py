@@ -132,7 +132,7 @@ def _check_status(status, what):
         raise errors.NonFinite(f"{what} produced a non-finite value")
 
 
-def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False):
+def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=None):
     """Reduce each fibre (seg_nodes[i] consecutive nodes) to one node."""
     torch = _torch()
     lib = _native.load()
@@ -143,7 +143,10 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False):
     scr = _Scratch(torch, level.ntot, dev, tdt, vdts)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     seg_nodes = np.asarray(seg_nodes, dtype=np.int64)
-    leaves = np.ones(int(seg_nodes.sum()), dtype=np.int64) if moments else None
+    leaves = None
+    if moments:
+        leaves = (np.asarray(leaves0, dtype=np.int64).copy() if leaves0 is not None
+                  else np.ones(int(seg_nodes.sum()), dtype=np.int64))
     while (seg_nodes > 1).any():
         src, cnt, nxt = _pairing(seg_nodes)
         nout = src.shape[0]

@@ -128,3 +128,25 @@ def test_mean_along_batched():
     assert tuple(M0.shape) == (9,)
     for c in range(9):
         assert M0[c] == pb.mean([A[r, c] for r in range(3)])
+
+
+def test_distributed_reductions_single_rank_match(tmp_path):
+    """mean_distributed / std_distributed (world 1, gloo) == single-GPU results."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_07183_b200 import datagen as dg, parallel
+    from paper_2404_07183_b200.reduce import DeviceLevel, mean_packed, std_packed
+
+    shape, mats = dg.noisy_trig_matrices((37,), 20, "sin", 0.1, dg.RngSpec(4))
+    t, v, off = dg.pack_matrices(mats)
+    dist.init_process_group("gloo", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    try:
+        m = parallel.mean_distributed(t, v, off, "cuda")
+        s = parallel.std_distributed(t, v, off, "cuda")
+    finally:
+        dist.destroy_process_group()
+    lvl = DeviceLevel.from_packed(t, v, off)
+    m1, s1 = mean_packed(lvl), std_packed(lvl)
+    assert torch.equal(m.t[: m.ntot], m1.t[: m1.ntot]) and torch.equal(m.v[: m.ntot], m1.v[: m1.ntot])
+    assert torch.equal(s.v[: s.ntot], s1.v[: s1.ntot])
