@@ -162,6 +162,17 @@ int pcf_compact(int is_f32, const void* st_dev, const void* sv_dev, const void* 
                 const int64_t* src_dev, int64_t nout, int64_t* pos_dev, void* temp_dev,
                 int64_t temp_bytes, void* t_out_dev, void* v_out_dev, void* v2_out_dev,
                 int64_t* off_out_dev, void* stream);
+/* Whole tree level, tiled two-pass (count -> tile scan -> write); replaces
+ * merge + compact.  kind 0..3 = add/max/min/mul on v (the PCFs' kind); 4 = moments
+ * (v = mean, v2 = M2, both float64; leaves_dev = leaf counts per input node).  Writes
+ * t_out/v_out(/v2_out) and off_out[nout+1]; workspace from pcf_tree_level_workspace. */
+int pcf_tree_level_workspace(int64_t ntot, int64_t* bytes);
+int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
+                   const double* v2_dev, const int64_t* off_dev, const int64_t* src_dev,
+                   const int32_t* cnt_dev, const int64_t* leaves_dev, int64_t nout,
+                   int64_t ntot, void* t_out_dev, void* v_out_dev, double* v2_out_dev,
+                   int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, int32_t* status_dev,
+                   void* stream);
 /* mean finalisation: v * T(scale[seg]) (core.scale) + keep-where-changed flags. */
 int pcf_scale_flag(int is_f32, const void* v_dev, const int64_t* off_dev, int64_t nseg,
                    const double* scale_dev, int64_t ntot, void* sv_dev, int32_t* flag_dev,

@@ -81,6 +81,10 @@ SIGNATURES = {
     "pcf_compact": (
         c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64,
                 c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pcf_tree_level_workspace": (c_int, [c_i64, c_i64p]),
+    "pcf_tree_level": (
+        c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+                c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pcf_scale_flag": (c_int, [c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "pcf_std_flag": (c_int, [c_int, c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
                              c_vp]),

@@ -132,63 +132,80 @@ def _check_status(status, what):
         raise errors.NonFinite(f"{what} produced a non-finite value")
 
 
-def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=None):
-    """Reduce each fibre (seg_nodes[i] consecutive nodes) to one node."""
-    torch = _torch()
-    lib = _native.load()
-    dev = level.t.device
-    st = current_stream_handle()
-    tdt = torch.float32 if level.is_f32 else torch.float64
-    vdts = [torch.float64, torch.float64] if moments else [tdt]
-    scr = _Scratch(torch, level.ntot, dev, tdt, vdts)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
+def _plan_levels(seg_nodes, leaves0=None, moments=False):
+    """All levels' (src, cnt[, leaves]) for fibres of seg_nodes nodes (host, once)."""
     seg_nodes = np.asarray(seg_nodes, dtype=np.int64)
     leaves = None
     if moments:
         leaves = (np.asarray(leaves0, dtype=np.int64).copy() if leaves0 is not None
                   else np.ones(int(seg_nodes.sum()), dtype=np.int64))
+    plan = []
     while (seg_nodes > 1).any():
         src, cnt, nxt = _pairing(seg_nodes)
-        nout = src.shape[0]
-        src_d = torch.from_numpy(src).to(dev)
-        cnt_d = torch.from_numpy(cnt).to(dev)
-        n = level.ntot
-        if moments:
-            leaves_d = torch.from_numpy(leaves).to(dev)
-            _native.check(lib.pcf_level_moments(
-                int(level.is_f32), _native.ptr(level.t), _native.ptr(level.v),
-                _native.ptr(level.m2), _native.ptr(level.off), _native.ptr(src_d),
-                _native.ptr(cnt_d), _native.ptr(leaves_d), nout, n, _native.ptr(scr.st),
-                _native.ptr(scr.sv[0]), _native.ptr(scr.sv[1]), _native.ptr(scr.flag), st),
-                "pcf_level_moments")
-        else:
-            _native.check(lib.pcf_level_merge(
-                int(op), int(level.is_f32), _native.ptr(level.t), _native.ptr(level.v),
-                _native.ptr(level.off), _native.ptr(src_d), _native.ptr(cnt_d), nout, n,
-                _native.ptr(scr.st), _native.ptr(scr.sv[0]), _native.ptr(scr.flag),
-                _native.ptr(status), st), "pcf_level_merge")
-        t_out = torch.empty_like(level.t)
-        v_out = torch.empty_like(level.v)
-        m2_out = torch.empty_like(level.m2) if moments else None
-        off_out = torch.empty(nout + 1, dtype=torch.int64, device=dev)
-        _native.check(lib.pcf_compact(
-            int(level.is_f32), _native.ptr(scr.st), _native.ptr(scr.sv[0]),
-            _native.ptr(scr.sv[1]) if moments else None,
-            8 if (moments or not level.is_f32) else 4, _native.ptr(scr.flag), n,
-            _native.ptr(level.off), _native.ptr(src_d), nout, _native.ptr(scr.pos),
-            _native.ptr(scr.temp), scr.temp.numel(), _native.ptr(t_out), _native.ptr(v_out),
-            _native.ptr(m2_out) if moments else None, _native.ptr(off_out), st), "pcf_compact")
-        ntot = int(off_out[-1].item())
-        level = DeviceLevel(t_out, v_out, off_out, nout, ntot, level.is_f32, m2_out)
+        plan.append((src, cnt, leaves))
         if moments:
             merged = leaves[src].copy()
             two = cnt == 2
             merged[two] += leaves[src[two] + 1]
             leaves = merged
         seg_nodes = nxt
+    return plan, leaves
+
+
+def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=None):
+    """Reduce each fibre (seg_nodes[i] consecutive nodes) to one node: one tiled
+    two-pass level kernel per tree level (pcf_tree_level).  The whole pairing plan is
+    uploaded once and the levels run back to back with no host synchronisation (each
+    level's point count is read on the device; the host passes an upper bound)."""
+    torch = _torch()
+    lib = _native.load()
+    dev = level.t.device
+    st = current_stream_handle()
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    plan, leaves_final = _plan_levels(seg_nodes, leaves0, moments)
+    if not plan:
+        return level, leaves_final
+    # one upload for every level's src / cnt (/ leaves)
+    src_all = np.concatenate([p[0] for p in plan])
+    cnt_all = np.concatenate([p[1] for p in plan])
+    src_d = torch.from_numpy(src_all).to(dev)
+    cnt_d = torch.from_numpy(cnt_all).to(dev)
+    if moments:
+        lv_all = np.concatenate([p[2] for p in plan])
+        lv_d = torch.from_numpy(lv_all).to(dev)
+    bound = max(level.ntot, 1)
+    nb = _native.c_i64(0)
+    lib.pcf_tree_level_workspace(bound, _native.ctypes.byref(nb))
+    ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=dev)
+    kind = 4 if moments else int(op)
+    bufs = [(torch.empty(bound, dtype=level.t.dtype, device=dev),
+             torch.empty(bound, dtype=level.v.dtype, device=dev),
+             torch.empty(bound, dtype=torch.float64, device=dev) if moments else None)
+            for _ in range(2)]
+    so = lo = 0
+    cur_t, cur_v, cur_m2, cur_off = level.t, level.v, level.m2, level.off
+    nout = level.nnodes
+    for li, (src, cnt, _) in enumerate(plan):
+        nout = src.shape[0]
+        t_out, v_out, m2_out = bufs[li % 2]
+        off_out = torch.empty(nout + 1, dtype=torch.int64, device=dev)
+        _native.check(lib.pcf_tree_level(
+            kind, int(level.is_f32), _native.ptr(cur_t), _native.ptr(cur_v),
+            _native.ptr(cur_m2) if moments else None, _native.ptr(cur_off),
+            _native.c_vp(src_d.data_ptr() + 8 * so), _native.c_vp(cnt_d.data_ptr() + 4 * so),
+            _native.c_vp(lv_d.data_ptr() + 8 * lo) if moments else None,
+            nout, bound, _native.ptr(t_out), _native.ptr(v_out),
+            _native.ptr(m2_out) if moments else None, _native.ptr(off_out), _native.ptr(ws),
+            ws.numel(), _native.ptr(status), st), "pcf_tree_level")
+        so += nout
+        if moments:
+            lo += plan[li][2].shape[0]
+        cur_t, cur_v, cur_m2, cur_off = t_out, v_out, m2_out, off_out
+    ntot = int(cur_off[-1].item())
     if not moments:
         _check_status(status, "reduction")
-    return level, leaves
+    out = DeviceLevel(cur_t, cur_v, cur_off, nout, ntot, level.is_f32, cur_m2)
+    return out, leaves_final
 
 
 def _finalize(level: DeviceLevel, scales, kind, take_sqrt=False):
