@@ -272,9 +272,9 @@ def run_ours(args):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
             rc = lib.pcf_fill_matrix(
-                _native.ptr(coll.recs), _native.ptr(coll.recs8), _native.ptr(coll.soff),
-                _native.ptr(coll.goff8), _native.ptr(coll.perm), M,
-                _native.c_vp(items_dev.data_ptr() + lo * 32), cnt, smem, mode,
+                _native.ptr(coll.tile_recs), _native.ptr(coll.recsg), _native.ptr(coll.soff),
+                _native.ptr(coll.goff), _native.ptr(coll.perm), M,
+                _native.c_vp(items_dev.data_ptr() + lo * 32), cnt, smem, mode, coll.rec_bytes,
                 _native.ptr(counter), 0, 1.0, 1, 0.0, math.inf, _native.ptr(out), 0, M,
                 _native.ptr(err), st)
             _native.check(rc, "pcf_fill_matrix")
@@ -456,16 +456,18 @@ def _build_collection(coll, dt, dv, do, off_host, dev):
     coll.soff = torch.from_numpy(soff).to(dev, non_blocking=True)
     coll.inv = None
     coll.recs = torch.empty(2 * coll.n_points, dtype=torch.float64, device=dev)
-    goff8 = np.zeros((M + 7) // 8 + 1, dtype=np.int64)
-    goff8[1:] = np.cumsum(8 * ssizes[0::8])
-    coll.goff8_host = goff8
-    coll.goff8 = torch.from_numpy(goff8).to(dev, non_blocking=True)
-    coll.recs8 = torch.empty(2 * int(goff8[-1]), dtype=torch.float64, device=dev)
+    goff = np.zeros((M + 7) // 8 + 1, dtype=np.int64)
+    goff[1:] = np.cumsum(8 * ssizes[0::8])
+    coll.rec_bytes = 16
+    coll.goff_host = goff
+    coll.goff = torch.from_numpy(goff).to(dev, non_blocking=True)
+    coll.recsg = torch.empty(2 * int(goff[-1]), dtype=torch.float64, device=dev)
+    coll.tile_recs = coll.recs
     coll._plans = {}
     _native.check(_native.load().pcf_pack_sorted(
         _native.ptr(dt), _native.ptr(dv), 0, _native.ptr(do), _native.ptr(coll.perm),
-        _native.ptr(coll.soff), M, _native.ptr(coll.recs), _native.ptr(coll.goff8),
-        _native.ptr(coll.recs8), current_stream_handle()), "pcf_pack_sorted")
+        _native.ptr(coll.soff), M, _native.ptr(coll.recs), _native.ptr(coll.goff),
+        _native.ptr(coll.recsg), current_stream_handle()), "pcf_pack_sorted")
 
 
 def main():

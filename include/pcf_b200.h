@@ -79,17 +79,27 @@ int pcf_pack_sorted(const void* tcat_dev, const void* vcat_dev, int is_f32,
  * record k of sorted PCF s lives at goff8[s/8] + 8k + s%8, so a quarter-warp reading the
  * 8 rows of one group always hits 8 distinct shared-memory bank groups.
  * goff8: int64[(M+7)/8 + 1], from pcf_group_offsets (host). */
-int pcf_group_offsets(const int64_t* sizes_sorted, int64_t M, int64_t* goff8);
+int pcf_group_offsets(const int64_t* sizes_sorted, int64_t M, int32_t group, int64_t* goff);
+/* float32 collections: 8-byte records {float t_next, float v} (the kernels widen them to
+ * float64 after the shared-memory load, as the reference widens every operand):
+ * recs32 = contiguous sorted records (allocate soff[M] + 2 records), recs32g = the
+ * 16-row slot-interleaved copy (goff16 from pcf_group_offsets(..., 16, ...)). */
+int pcf_pack_sorted32(const float* tcat_dev, const float* vcat_dev, const int64_t* off_dev,
+                      const int32_t* perm_dev, const int64_t* soff_dev, int64_t M,
+                      void* recs32_dev, const int64_t* goff16_dev, void* recs32g_dev,
+                      void* stream);
 
 /* ---- planner (host): sizes in sorted order -> work items, cost-descending ---- */
 /* Returns the dynamic shared memory the items need in *smem_bytes.  `items` may be NULL
  * to query the count.  max_cols bounds the columns per item (load-balance granularity).
+ * rec_bytes: 16 (float64 records, 8-row groups) or 8 (float32 records, 16-row groups).
  * max_log2G caps the merge-path split: 0 = one lane per pair everywhere, which sums every
  * entry strictly left to right exactly like the reference (bitwise for p=1 and INNER);
  * 6 = up to 64 segments per pair (fastest; same cell products, summed in G runs). */
 int pcf_plan_pairwise(const int64_t* sizes_sorted, int64_t M, int64_t smem_budget,
-                      int64_t max_cols, int32_t max_log2G, pcf_work_item* items, int64_t cap,
-                      int64_t* n_items, int32_t* smem_bytes);
+                      int64_t max_cols, int32_t max_log2G, int32_t rec_bytes,
+                      pcf_work_item* items, int64_t cap, int64_t* n_items,
+                      int32_t* smem_bytes);
 
 /* ---- K1: whole upper triangle (diagonal excluded) of the pairwise matrix ---- */
 /* out_dev: M x M row-major (leading dim ld) float64 (out_is_f32=0) or float32; entries
@@ -99,7 +109,8 @@ int pcf_plan_pairwise(const int64_t* sizes_sorted, int64_t M, int64_t smem_budge
 int pcf_fill_matrix(const void* recs_dev, const void* recs8_dev, const int64_t* soff_dev,
                     const int64_t* goff8_dev, const int32_t* perm_dev,
                     int64_t M, const pcf_work_item* items_dev, int64_t n_items,
-                    int32_t smem_bytes, int32_t smem_mode, int32_t* counter_dev, int op,
+                    int32_t smem_bytes, int32_t smem_mode, int32_t rec_bytes,
+                    int32_t* counter_dev, int op,
                     double p, int apply_root, double a, double b, void* out_dev,
                     int out_is_f32, int64_t ld, unsigned long long* err_dev, void* stream);
 

@@ -46,12 +46,14 @@ SIGNATURES = {
     "pcf_last_error": (ctypes.c_char_p, []),
     "pcf_tile_threads": (c_int, []),
     "pcf_pack_sorted": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
-    "pcf_group_offsets": (c_int, [c_vp, c_i64, c_vp]),
-    "pcf_plan_pairwise": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i32, c_vp, c_i64, c_i64p, c_i32p]),
+    "pcf_group_offsets": (c_int, [c_vp, c_i64, c_i32, c_vp]),
+    "pcf_pack_sorted32": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "pcf_plan_pairwise": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp, c_i64, c_i64p,
+                                  c_i32p]),
     "pcf_fill_matrix": (
         c_int,
-        [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_int, c_dbl, c_int,
-         c_dbl, c_dbl, c_vp, c_int, c_i64, c_vp, c_vp],
+        [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_int, c_dbl,
+         c_int, c_dbl, c_dbl, c_vp, c_int, c_i64, c_vp, c_vp],
     ),
     "pcf_fill_diagonal": (
         c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_dbl, c_dbl, c_vp, c_int, c_i64, c_vp, c_vp]

@@ -4,8 +4,10 @@ Layout in HBM:
 
 * ``recs``  float64[2*N]  -- N 16-byte records {t_next, v} in size-sorted order;
 * ``soff``  int64[M+1]    -- record offsets of sorted PCF s;
-* ``recs8`` / ``goff8``   -- the same records slot-interleaved in groups of 8 sorted PCFs
-  (record k of PCF s at goff8[s/8] + 8k + s%8), the layout K1 stages its row blocks in;
+* ``recsg`` / ``goff``    -- the K1 tile layout: the same records slot-interleaved in
+  groups of GW sorted PCFs (record k of PCF s at goff[s/GW] + GW*k + s%GW), the layout K1
+  stages its row blocks in; GW = 8 for float64 (16-byte records), 16 for float32
+  collections, which K1 reads as 8-byte float32 records (``tile_recs``);
 * ``perm``  int32[M]      -- sorted index -> original index;
 * ``inv``   int32[M]      -- original index -> sorted index.
 
@@ -72,10 +74,13 @@ class DeviceCollection:
         self.sizes_sorted = ssizes
         self.perm_host = perm
         self.n_points = int(soff[-1])
-        ng = (self.M + 7) // 8
-        goff8 = np.zeros(ng + 1, dtype=np.int64)
-        goff8[1:] = np.cumsum(8 * ssizes[0::8])
-        self.goff8_host = goff8
+        # K1 tile layout: float64 -> 16-byte records, 8-row interleaved groups;
+        # float32 -> 8-byte records, 16-row interleaved groups (half the shared-memory bytes)
+        self.rec_bytes = 8 if self.dtype == np.float32 else 16
+        gw = 128 // self.rec_bytes
+        goff = np.zeros((self.M + gw - 1) // gw + 1, dtype=np.int64)
+        goff[1:] = np.cumsum(gw * ssizes[0::gw])
+        self.goff_host = goff
         with torch.cuda.device(self.device):
             dev = self.device
             t_d = torch.from_numpy(tcat).to(dev, non_blocking=False)
@@ -85,14 +90,34 @@ class DeviceCollection:
             self.inv = torch.from_numpy(inv).to(dev)
             self.soff = torch.from_numpy(soff).to(dev)
             self.recs = torch.empty(2 * max(self.n_points, 1), dtype=torch.float64, device=dev)
-            self.goff8 = torch.from_numpy(goff8).to(dev)
-            self.recs8 = torch.empty(2 * max(int(goff8[-1]), 1), dtype=torch.float64, device=dev)
-            rc = lib.pcf_pack_sorted(
-                _native.ptr(t_d), _native.ptr(v_d), int(self.dtype == np.float32),
-                _native.ptr(off_d), _native.ptr(self.perm), _native.ptr(self.soff), self.M,
-                _native.ptr(self.recs), _native.ptr(self.goff8), _native.ptr(self.recs8),
-                current_stream_handle())
-            _native.check(rc, "pcf_pack_sorted")
+            self.goff = torch.from_numpy(goff).to(dev)
+            st = current_stream_handle()
+            if self.rec_bytes == 16:
+                self.recsg = torch.empty(2 * max(int(goff[-1]), 1), dtype=torch.float64,
+                                         device=dev)
+                rc = lib.pcf_pack_sorted(
+                    _native.ptr(t_d), _native.ptr(v_d), 0, _native.ptr(off_d),
+                    _native.ptr(self.perm), _native.ptr(self.soff), self.M,
+                    _native.ptr(self.recs), _native.ptr(self.goff), _native.ptr(self.recsg), st)
+                _native.check(rc, "pcf_pack_sorted")
+                self.tile_recs = self.recs
+            else:
+                rc = lib.pcf_pack_sorted(
+                    _native.ptr(t_d), _native.ptr(v_d), 1, _native.ptr(off_d),
+                    _native.ptr(self.perm), _native.ptr(self.soff), self.M,
+                    _native.ptr(self.recs), None, None, st)
+                _native.check(rc, "pcf_pack_sorted")
+                # +2 records: column chunks are copied in whole 16-byte units
+                self.tile_recs = torch.zeros(2 * (self.n_points + 2), dtype=torch.float32,
+                                             device=dev)
+                self.recsg = torch.empty(2 * max(int(goff[-1]), 1), dtype=torch.float32,
+                                         device=dev)
+                rc = lib.pcf_pack_sorted32(
+                    _native.ptr(t_d), _native.ptr(v_d), _native.ptr(off_d),
+                    _native.ptr(self.perm), _native.ptr(self.soff), self.M,
+                    _native.ptr(self.tile_recs), _native.ptr(self.goff),
+                    _native.ptr(self.recsg), st)
+                _native.check(rc, "pcf_pack_sorted32")
             del t_d, v_d, off_d
         self._plans = {}
 
@@ -118,6 +143,7 @@ class DeviceCollection:
         sum, bitwise for p=1 and inner products); otherwise up to a warp per pair."""
         max_log2g = 0 if exact else 6
         key = (max_log2g, smem_budget, max_cols)
+        rb = self.rec_bytes
         if key in self._plans:
             return self._plans[key]
         torch = _torch()
@@ -126,11 +152,13 @@ class DeviceCollection:
         n = ctypes.c_int64(0)
         smem = ctypes.c_int32(0)
         _native.check(lib.pcf_plan_pairwise(_native.ptr(sizes), self.M, smem_budget, max_cols,
-                                            max_log2g, None, 0, ctypes.byref(n), ctypes.byref(smem)),
+                                            max_log2g, rb, None, 0, ctypes.byref(n),
+                                            ctypes.byref(smem)),
                       "pcf_plan_pairwise")
         items = (_native.WorkItem * max(n.value, 1))()
         _native.check(lib.pcf_plan_pairwise(_native.ptr(sizes), self.M, smem_budget, max_cols,
-                                            max_log2g, ctypes.cast(items, ctypes.c_void_p), n.value,
+                                            max_log2g, rb, ctypes.cast(items, ctypes.c_void_p),
+                                            n.value,
                                             ctypes.byref(n), ctypes.byref(smem)),
                       "pcf_plan_pairwise")
         host = np.frombuffer(items, dtype=np.int32).reshape(-1, 8)[: n.value].copy()

@@ -57,15 +57,30 @@ int pcf_pack_sorted(const void* tcat_dev, const void* vcat_dev, int is_f32,
 // ------------------------------------------------------------------------------ planner
 // Offsets of the slot-interleaved 8-row groups (record k of sorted PCF s at
 // goff8[s/8] + 8k + s%8): group g spans 8 * sizes[8g] records (sizes sorted descending).
-int pcf_group_offsets(const int64_t* sizes, int64_t M, int64_t* goff8) {
-  if (M < 0 || (M > 0 && (!sizes || !goff8))) {
+int pcf_group_offsets(const int64_t* sizes, int64_t M, int32_t group, int64_t* goff) {
+  if (M < 0 || (M > 0 && (!sizes || !goff)) || (group != 8 && group != 16)) {
     set_error("pcf_group_offsets: bad arguments");
     return PCF_ERR_ARG;
   }
-  const int64_t ng = (M + 7) / 8;
-  goff8[0] = 0;
-  for (int64_t g = 0; g < ng; ++g) goff8[g + 1] = goff8[g] + 8 * sizes[8 * g];
+  const int64_t ng = (M + group - 1) / group;
+  goff[0] = 0;
+  for (int64_t g = 0; g < ng; ++g) goff[g + 1] = goff[g] + group * sizes[group * g];
   return PCF_OK;
+}
+
+int pcf_pack_sorted32(const float* tcat_dev, const float* vcat_dev, const int64_t* off_dev,
+                      const int32_t* perm_dev, const int64_t* soff_dev, int64_t M,
+                      void* recs32_dev, const int64_t* goff16_dev, void* recs32g_dev,
+                      void* stream) {
+  if (M <= 0) return PCF_OK;
+  if (!tcat_dev || !vcat_dev || !off_dev || !perm_dev || !soff_dev || !recs32_dev ||
+      !goff16_dev || !recs32g_dev) {
+    set_error("pcf_pack_sorted32: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  cudaError_t e = launch_pack32(tcat_dev, vcat_dev, off_dev, perm_dev, soff_dev, M, recs32_dev,
+                                goff16_dev, recs32g_dev, (cudaStream_t)stream);
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_pack_sorted32");
 }
 
 // Row blocks of the size-sorted collection are one or two 8-row groups.  Each gets the
@@ -76,9 +91,10 @@ int pcf_group_offsets(const int64_t* sizes, int64_t M, int64_t* goff8) {
 // columns; items are returned cost-descending (LPT order for the persistent kernels'
 // atomic queues), shared-memory items first.
 int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int64_t max_cols,
-                      int32_t max_log2G, pcf_work_item* items, int64_t cap, int64_t* n_items,
-                      int32_t* smem_bytes) {
-  if (M < 0 || (M > 0 && !sizes) || !n_items || smem_budget <= 0) {
+                      int32_t max_log2G, int32_t rec_bytes, pcf_work_item* items, int64_t cap,
+                      int64_t* n_items, int32_t* smem_bytes) {
+  if (M < 0 || (M > 0 && !sizes) || !n_items || smem_budget <= 0 ||
+      (rec_bytes != 8 && rec_bytes != 16)) {
     set_error("pcf_plan_pairwise: bad arguments");
     return PCF_ERR_ARG;
   }
@@ -90,10 +106,13 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     }
     S[i + 1] = S[i] + sizes[i];
   }
+  const int GW = 128 / rec_bytes;        // rows per interleaved group / lanes per smem phase
+  const int LOGU = GW == 16 ? 5 : 6;     // log2 of phase units per CTA (512 / GW)
+  const int64_t RB = rec_bytes;
   if (max_log2G < 0) max_log2G = 0;
-  if (max_log2G > 6) max_log2G = 6;
+  if (max_log2G > LOGU) max_log2G = LOGU;
   auto al = [](int64_t x) { return (x + 127) & ~(int64_t)127; };
-  auto group_recs = [&](int64_t r) { return 8 * sizes[r]; };  // r: first row of a group
+  auto group_recs = [&](int64_t r) { return (int64_t)GW * sizes[r]; };  // r: first row of a group
   const int T = kTileThreads;
   std::vector<pcf_work_item> smem_items, glob_items;
   int64_t need_max = 0;
@@ -103,15 +122,16 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     int best_logRG = -1, best_logC = 0, best_logG = 99;
     int64_t best_need = 0;
     for (int logRG = 1; logRG >= 0; --logRG) {
-      if (logRG == 1 && r0 + 8 >= M - 1) continue;  // second group would be empty of pairs
-      int64_t rows_b = group_recs(r0) * 16;
-      if (logRG == 1) rows_b += group_recs(r0 + 8) * 16;
-      for (int logC = 6 - logRG; logC >= 0; --logC) {
-        const int logG = 6 - logRG - logC;
+      if (logRG == 1 && r0 + GW >= M - 1) continue;  // second group would have no pairs
+      int64_t rows_b = group_recs(r0) * RB;
+      if (logRG == 1) rows_b += group_recs(r0 + GW) * RB;
+      for (int logC = LOGU - logRG; logC >= 0; --logC) {
+        const int logG = LOGU - logRG - logC;
         if (logG > max_log2G) break;
         const int64_t C = 1 << logC;
         const int64_t c0 = r0 + 1, ce = std::min<int64_t>(c0 + C, M);
-        const int64_t need = al(rows_b) + 2 * al((S[ce] - S[c0]) * 16) + kRedBytes;
+        const int64_t need =
+            al(rows_b) + 2 * al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
         if (need > smem_budget) continue;
         if (logG < best_logG || (logG == best_logG && logRG > best_logRG)) {
           best_logRG = logRG;
@@ -122,16 +142,16 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
         break;  // larger logC with this RG already failed or this one fits; keep smallest G
       }
     }
-    const bool smem = best_logRG >= 0 && (r0 % 8) == 0;
+    const bool smem = best_logRG >= 0 && (r0 % GW) == 0;
     int rows, logC, logG;
     if (smem) {
-      rows = 8 << best_logRG;
+      rows = GW << best_logRG;
       logC = best_logC;
       logG = best_logG;
     } else {  // rows too long to stage: operands from L1/L2, G lanes in one warp
       logG = std::min(max_log2G, 5);
       const int P = T >> logG;
-      rows = P <= 64 ? 8 : 32;
+      rows = P <= 64 ? GW : 32;
       logC = 0;
       while ((rows << (logC + 1)) <= P) ++logC;
     }
@@ -178,7 +198,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
 int pcf_fill_matrix(const void* recs_dev, const void* recs8_dev, const int64_t* soff_dev,
                     const int64_t* goff8_dev, const int32_t* perm_dev,
                     int64_t M, const pcf_work_item* items_dev, int64_t n_items,
-                    int32_t smem_bytes, int32_t smem_mode, int32_t* counter_dev, int op,
+                    int32_t smem_bytes, int32_t smem_mode, int32_t rec_bytes,
+                    int32_t* counter_dev, int op,
                     double p, int apply_root, double a, double b, void* out_dev,
                     int out_is_f32, int64_t ld, unsigned long long* err_dev, void* stream) {
   if (n_items <= 0) return PCF_OK;
@@ -213,6 +234,7 @@ int pcf_fill_matrix(const void* recs_dev, const void* recs8_dev, const int64_t* 
   A.err = err_dev;
   A.smem_mode = smem_mode;
   A.smem_bytes = smem_bytes;
+  A.rec_bytes = rec_bytes == 8 ? 8 : 16;
   A.num_sms = num_sms_current();
   e = launch_fill_tiles(A, st);
   return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_fill_matrix");

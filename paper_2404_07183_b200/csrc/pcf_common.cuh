@@ -19,6 +19,13 @@ struct __align__(16) Rec {
   double v;  // value on this piece
 };
 
+// 8-byte record for float32 collections (the reference widens every operand to float64
+// before any arithmetic, pyx:38-41; so do the kernels, after the shared-memory load).
+struct __align__(8) Rec32 {
+  float t;
+  float v;
+};
+
 // Integrand kinds.  OP_LP with p=1/2/3 get exact-arithmetic specialisations; any
 // other p goes through pow().  OP_INNER is v_f * v_g.
 enum HKind { H_L1 = 0, H_L2 = 1, H_L3 = 2, H_LP = 3, H_INNER = 4 };

@@ -29,6 +29,7 @@ struct FillArgs {
   unsigned long long* err;
   int smem_mode;
   int smem_bytes;
+  int rec_bytes;  // 16: float64 records, 8: float32 records (recs/recs8 point to Rec32)
   int num_sms;
 };
 
@@ -57,6 +58,10 @@ cudaError_t launch_pair_list(const void* recs, const int64_t* soff, const int64_
 cudaError_t launch_pack(const void* tcat, const void* vcat, int f32, const int64_t* off,
                         const int32_t* perm, const int64_t* soff, int64_t M, void* recs,
                         const int64_t* goff8, void* recs8, cudaStream_t st);
+
+cudaError_t launch_pack32(const float* tcat, const float* vcat, const int64_t* off,
+                          const int32_t* perm, const int64_t* soff, int64_t M, void* recs32,
+                          const int64_t* goff16, void* recs32g, cudaStream_t st);
 
 constexpr int kRedBytes = 4 * kTileThreads * 8;  // K1 segment partials + tails, 2 buffers
 

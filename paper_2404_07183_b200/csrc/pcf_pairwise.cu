@@ -34,17 +34,17 @@ namespace pcfb {
 // Bounded b: cell right edges are clamped to b (cells past b become zero-width) and the
 // last lane adds the final cell h(v_f_last, v_g_last) * (b - t).  Unbounded b: the tail
 // cell is left to the caller, which applies the divergence rule of pyx:47-51.
-template <int HK, bool BOUNDED, int SF, int SG>
-__device__ __forceinline__ double lane_walk(const Rec* __restrict__ F, int nf,
-                                            const Rec* __restrict__ Gv, int ng, int lane,
+template <int HK, bool BOUNDED, int SF, int SG, typename RT = Rec>
+__device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
+                                            const RT* __restrict__ Gv, int ng, int lane,
                                             int log2G, double p, double a, double b) {
   int k0 = 0, m0 = 0;
   if (a > 0.0) {  // start cursors k = max{i : t_i <= a} (pyx:33-36), by binary search
     k0 = upper_bound_count(nf - 1, a, [&](int x) { return F[x * SF].t; });
     m0 = upper_bound_count(ng - 1, a, [&](int x) { return Gv[x * SG].t; });
   }
-  const Rec* __restrict__ Fk = F + k0 * SF;
-  const Rec* __restrict__ Gm = Gv + m0 * SG;
+  const RT* __restrict__ Fk = F + k0 * SF;
+  const RT* __restrict__ Gm = Gv + m0 * SG;
   const int Nf = nf - 1 - k0, Ng = ng - 1 - m0;
   const int N = Nf + Ng;
   const int d0 = (int)(((long long)lane * N) >> log2G);
@@ -61,8 +61,8 @@ __device__ __forceinline__ double lane_walk(const Rec* __restrict__ F, int nf,
   if (d0 == 0) {
     t = a;
   } else {
-    const double tfp = i > 0 ? Fk[(i - 1) * SF].t : 0.0;
-    const double tgp = j > 0 ? Gm[(j - 1) * SG].t : 0.0;
+    const double tfp = i > 0 ? (double)Fk[(i - 1) * SF].t : 0.0;
+    const double tgp = j > 0 ? (double)Gm[(j - 1) * SG].t : 0.0;
     t = fmax(tfp, tgp);
   }
   if (BOUNDED) t = fmin(t, b);
@@ -70,28 +70,31 @@ __device__ __forceinline__ double lane_walk(const Rec* __restrict__ F, int nf,
   // is symmetric in (v_f, v_g), so the cell needs no f/g identity: tn = tX, advance X,
   // then swap roles if the new X piece outlasts Y.  (Ties may be taken in either order:
   // the extra zero-width cell adds +-0.)
-  const Rec* __restrict__ xp = Fk + i * SF;
-  const Rec* __restrict__ yp = Gm + j * SG;
+  // The cursor state keeps the stored scalar kind (float for 8-byte records: half the
+  // register moves per swap); every operand is widened to float64 before arithmetic.
+  using ST = decltype(RT::t);
+  const RT* __restrict__ xp = Fk + i * SF;
+  const RT* __restrict__ yp = Gm + j * SG;
   int xs = SF, ys = SG;
-  double tx = xp->t, vx = xp->v, ty = yp->t, vy = yp->v;
+  ST tx = xp->t, vx = xp->v, ty = yp->t, vy = yp->v;
   if (ty < tx) {
-    const Rec* tp = xp; xp = yp; yp = tp;
+    const RT* tp = xp; xp = yp; yp = tp;
     int ts = xs; xs = ys; ys = ts;
-    double tt = tx; tx = ty; ty = tt;
+    ST tt = tx; tx = ty; ty = tt;
     tt = vx; vx = vy; vy = tt;
   }
   double acc = 0.0;
   const int steps = d1 - d0;
 #pragma unroll 4
   for (int s = 0; s < steps; ++s) {
-    double tn = tx;
+    double tn = (double)tx;
     if (BOUNDED) tn = fmin(tn, b);
-    acc = __dadd_rn(acc, __dmul_rn(hval<HK>(vx, vy, p), __dsub_rn(tn, t)));
+    acc = __dadd_rn(acc, __dmul_rn(hval<HK>((double)vx, (double)vy, p), __dsub_rn(tn, t)));
     t = tn;
     xp += xs;
-    const double nt = xp->t, nv = xp->v;
+    const ST nt = xp->t, nv = xp->v;
     const bool sw = nt > ty;
-    const Rec* __restrict__ np = sw ? yp : xp;
+    const RT* __restrict__ np = sw ? yp : xp;
     yp = sw ? xp : yp;
     xp = np;
     if (SF != SG) {
@@ -105,7 +108,7 @@ __device__ __forceinline__ double lane_walk(const Rec* __restrict__ F, int nf,
     vy = sw ? nv : vy;
   }
   if (BOUNDED && (lane == (1 << log2G) - 1)) {
-    acc = __dadd_rn(acc, __dmul_rn(hval<HK>(vx, vy, p), __dsub_rn(b, t)));
+    acc = __dadd_rn(acc, __dmul_rn(hval<HK>((double)vx, (double)vy, p), __dsub_rn(b, t)));
   }
   return acc;
 }
@@ -145,14 +148,18 @@ __device__ __forceinline__ void finish_entry(double acc, double hl, double p, in
 // 64 quarters = RG row groups x C columns x G merge-path segments.  With G > 1 the
 // segment partials go through shared memory and one thread per pair adds them in
 // segment order.
-template <int HK, bool BOUNDED, typename OutT>
+template <int HK, bool BOUNDED, typename OutT, typename RT, int GW>
 __global__ void __launch_bounds__(kTileThreads, 1)
-    k_fill_tiles_smem(const Rec* __restrict__ recs, const Rec* __restrict__ recs8,
-                      const int64_t* __restrict__ soff, const int64_t* __restrict__ goff8,
+    k_fill_tiles_smem(const RT* __restrict__ recs, const RT* __restrict__ recsg,
+                      const int64_t* __restrict__ soff, const int64_t* __restrict__ goff,
                       const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
                       int n_items, int* __restrict__ counter, double p, double a, double b,
                       int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
                       unsigned long long* __restrict__ err) {
+  // GW: rows per interleaved group = lanes per shared-memory phase for sizeof(RT)-byte
+  // loads (8 x 16 B or 16 x 8 B = 128 B); CA: records per 16 B (bulk-copy granularity)
+  constexpr int LOGGW = GW == 16 ? 4 : 3;
+  constexpr int CA = 16 / (int)sizeof(RT);
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[3];  // 0: rows, 1/2: column buffers
   __shared__ int s_item;
@@ -165,6 +172,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   }
   __syncthreads();
   uint32_t ph_row = 0, ph_col[2] = {0u, 0u};
+  auto cstart = [&](int c0) { const int64_t r = soff[c0]; return r - r % CA; };
+  auto cend = [&](int c1) { const int64_t r = soff[c1]; return (r + CA - 1) / CA * CA; };
 
   for (;;) {
     if (tid == 0) s_item = atomicAdd(counter, 1);
@@ -172,14 +181,15 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const int it = s_item;
     if (it >= n_items) break;
     const PcfWorkItem W = items[it];
-    const int logRG = W.nrows > 8 ? 1 : 0;
+    const int logRG = W.nrows > GW ? 1 : 0;
     const int RG = 1 << logRG, C = 1 << W.logC, log2G = W.log2G, G = 1 << log2G;
-    const int rg0 = W.row0 >> 3;
-    const int64_t rbase = goff8[rg0];
-    const uint32_t row_bytes = (uint32_t)((goff8[rg0 + RG] - rbase) * sizeof(Rec));
+    const int rg0 = W.row0 >> LOGGW;
+    const int64_t rbase = goff[rg0];
+    const uint32_t row_bytes = (uint32_t)((goff[rg0 + RG] - rbase) * sizeof(RT));
     const int nchunk = (W.col1 - W.col0 + C - 1) >> W.logC;
     const int c_first_end = min(W.col0 + C, W.col1);
-    const uint32_t col_cap = (uint32_t)((soff[c_first_end] - soff[W.col0]) * sizeof(Rec));
+    const uint32_t col_cap =
+        (uint32_t)((cend(c_first_end) - cstart(W.col0)) * sizeof(RT)) + 16u;
     const uint32_t row_al = (row_bytes + 127u) & ~127u;
     const uint32_t col_al = (col_cap + 127u) & ~127u;
     unsigned char* rowbuf = smem;
@@ -190,31 +200,32 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     if (tid == 0) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], row_bytes);
-      bulk_g2s(rowbuf, recs8 + rbase, row_bytes, &bars[0]);
+      bulk_g2s(rowbuf, recsg + rbase, row_bytes, &bars[0]);
       for (int c = 0; c < 2 && c < nchunk; ++c) {
         const int cb = W.col0 + (c << W.logC), ce = min(cb + C, W.col1);
-        const uint32_t nb = (uint32_t)((soff[ce] - soff[cb]) * sizeof(Rec));
+        const int64_t r0 = cstart(cb);
+        const uint32_t nb = (uint32_t)((cend(ce) - r0) * sizeof(RT));
         mbar_arrive_expect_tx(&bars[1 + c], nb);
-        bulk_g2s(colbase + c * col_al, recs + soff[cb], nb, &bars[1 + c]);
+        bulk_g2s(colbase + c * col_al, recs + r0, nb, &bars[1 + c]);
       }
     }
     // lane -> (row slot u, row group rho, column cc, segment g); fixed for the item
-    const int u = tid & 7;
-    const int Q = tid >> 3;
+    const int u = tid & (GW - 1);
+    const int Q = tid >> LOGGW;
     const int rho = Q & (RG - 1);
     const int cc = (Q >> logRG) & (C - 1);
     const int g = Q >> (logRG + W.logC);
-    const int ps = W.row0 + 8 * rho + u;
+    const int ps = W.row0 + GW * rho + u;
     const bool row_ok = ps < M;
     int nf = 0;
-    const Rec* F = reinterpret_cast<const Rec*>(rowbuf) + (goff8[rg0 + rho] - rbase) + u;
+    const RT* F = reinterpret_cast<const RT*>(rowbuf) + (goff[rg0 + rho] - rbase) + u;
     int64_t oi = 0;
     if (row_ok) {
       nf = (int)(soff[ps + 1] - soff[ps]);
       oi = perm[ps];
     }
-    const int pair_id = (cc * RG + rho) * 8 + u;  // 0 .. 8*RG*C-1
-    const int npairs = 8 * RG * C;
+    const int pair_id = (cc * RG + rho) * GW + u;  // 0 .. GW*RG*C-1
+    const int npairs = GW * RG * C;
     mbar_wait(&bars[0], ph_row);
     ph_row ^= 1u;
 
@@ -226,13 +237,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const bool ok = row_ok && qs < ce && qs > ps;
       mbar_wait(&bars[1 + buf], ph_col[buf]);
       ph_col[buf] ^= 1u;
-      const Rec* Gv = reinterpret_cast<const Rec*>(colbase + buf * col_al);
+      const RT* Gv = reinterpret_cast<const RT*>(colbase + buf * col_al);
       double acc = 0.0, hl = 0.0;
       if (ok) {
         const int ng = (int)(soff[qs + 1] - soff[qs]);
-        Gv += soff[qs] - soff[cb];
-        acc = lane_walk<HK, BOUNDED, 8, 1>(F, nf, Gv, ng, g, log2G, p, a, b);
-        if (!BOUNDED) hl = hval<HK>(F[(nf - 1) * 8].v, Gv[ng - 1].v, p);
+        Gv += soff[qs] - cstart(cb);
+        acc = lane_walk<HK, BOUNDED, GW, 1, RT>(F, nf, Gv, ng, g, log2G, p, a, b);
+        if (!BOUNDED) hl = hval<HK>(F[(nf - 1) * GW].v, Gv[ng - 1].v, p);
       }
       if (G == 1) {
         if (ok) finish_entry<BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
@@ -242,8 +253,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         if (g == 0) redh[buf * kTileThreads + pair_id] = hl;
         __syncthreads();  // partials visible, buffer `buf` free again
         if (tid < npairs) {
-          const int pu = tid & 7, prho = (tid >> 3) & (RG - 1), pcc = tid >> (3 + logRG);
-          const int pps = W.row0 + 8 * prho + pu, pqs = cb + pcc;
+          const int pu = tid & (GW - 1), prho = (tid >> LOGGW) & (RG - 1);
+          const int pcc = tid >> (LOGGW + logRG);
+          const int pps = W.row0 + GW * prho + pu, pqs = cb + pcc;
           if (pps < M && pqs < ce && pqs > pps) {
             const double* r = red + buf * kTileThreads + tid;
             double s = r[0];
@@ -255,10 +267,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       }
       if (tid == 0 && c + 2 < nchunk) {
         const int nb0 = W.col0 + ((c + 2) << W.logC), ne = min(nb0 + C, W.col1);
-        const uint32_t nb = (uint32_t)((soff[ne] - soff[nb0]) * sizeof(Rec));
+        const int64_t r0 = cstart(nb0);
+        const uint32_t nb = (uint32_t)((cend(ne) - r0) * sizeof(RT));
         fence_proxy_async();
         mbar_arrive_expect_tx(&bars[1 + buf], nb);
-        bulk_g2s(colbase + buf * col_al, recs + soff[nb0], nb, &bars[1 + buf]);
+        bulk_g2s(colbase + buf * col_al, recs + r0, nb, &bars[1 + buf]);
       }
     }
     __syncthreads();  // all finishers done before the next item reuses shared memory
@@ -268,9 +281,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // K1g: tiles whose PCFs are too long to stage; operands read straight from the
 // contiguous records through L1/L2.  R x C pairs per pass, G lanes per pair in one warp
 // (butterfly reduction).
-template <int HK, bool BOUNDED, typename OutT>
+template <int HK, bool BOUNDED, typename OutT, typename RT>
 __global__ void __launch_bounds__(kTileThreads, 1)
-    k_fill_tiles_global(const Rec* __restrict__ recs, const int64_t* __restrict__ soff,
+    k_fill_tiles_global(const RT* __restrict__ recs, const int64_t* __restrict__ soff,
                         const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
                         int n_items, int* __restrict__ counter, double p, double a, double b,
                         int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
@@ -295,13 +308,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const int qs = cb + cc;
       const bool ok = row_ok && qs < W.col1 && qs > ps;
       double acc = 0.0;
-      const Rec* F = recs + (row_ok ? soff[ps] : 0);
-      const Rec* Gv = recs + (ok ? soff[qs] : 0);
+      const RT* F = recs + (row_ok ? soff[ps] : 0);
+      const RT* Gv = recs + (ok ? soff[qs] : 0);
       int nf = 0, ng = 0;
       if (ok) {
         nf = (int)(soff[ps + 1] - soff[ps]);
         ng = (int)(soff[qs + 1] - soff[qs]);
-        acc = lane_walk<HK, BOUNDED, 1, 1>(F, nf, Gv, ng, lane, log2G, p, a, b);
+        acc = lane_walk<HK, BOUNDED, 1, 1, RT>(F, nf, Gv, ng, lane, log2G, p, a, b);
       }
       for (int o = (1 << log2G) >> 1; o >= 1; o >>= 1)
         acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
@@ -450,6 +463,43 @@ __global__ void k_pack_sorted(const T* __restrict__ tcat, const T* __restrict__ 
   }
 }
 
+// float32 collections: 8-byte records, contiguous (+ CA-aligned tail) and slot-interleaved
+// in groups of 16 (record k of sorted PCF s at goff16[s/16] + 16k + s%16).
+__global__ void k_pack_sorted32(const float* __restrict__ tcat, const float* __restrict__ vcat,
+                                const int64_t* __restrict__ off, const int32_t* __restrict__ perm,
+                                const int64_t* __restrict__ soff, int64_t M,
+                                Rec32* __restrict__ recs, const int64_t* __restrict__ goff16,
+                                Rec32* __restrict__ recsg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = w0; s < M; s += nw) {
+    const int64_t o = perm[s];
+    const int64_t src = off[o];
+    const int64_t n = off[o + 1] - src;
+    Rec32* dst = recs + soff[s];
+    Rec32* dstg = recsg + goff16[s >> 4] + (s & 15);
+    for (int64_t k = lane; k < n; k += 32) {
+      Rec32 r;
+      r.t = (k + 1 < n) ? tcat[src + k + 1] : INFINITY;
+      r.v = vcat[src + k];
+      dst[k] = r;
+      dstg[16 * k] = r;
+    }
+  }
+}
+
+cudaError_t launch_pack32(const float* tcat, const float* vcat, const int64_t* off,
+                          const int32_t* perm, const int64_t* soff, int64_t M, void* recs32,
+                          const int64_t* goff16, void* recs32g, cudaStream_t st) {
+  int grid = (int)((M * 32 + 255) / 256);
+  if (grid > 148 * 64) grid = 148 * 64;
+  if (grid < 1) grid = 1;
+  k_pack_sorted32<<<grid, 256, 0, st>>>(tcat, vcat, off, perm, soff, M, (Rec32*)recs32, goff16,
+                                        (Rec32*)recs32g);
+  return cudaGetLastError();
+}
+
 // ======================================================================================
 // launch helpers (called from the C-ABI layer)
 
@@ -457,15 +507,28 @@ template <int HK, bool BOUNDED, typename OutT>
 static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
   const int grid = A.num_sms;  // persistent: one CTA per SM
   if (A.smem_mode) {
-    auto kern = k_fill_tiles_smem<HK, BOUNDED, OutT>;
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
-        (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
-        A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+    cudaError_t e;
+    if (A.rec_bytes == 8) {
+      auto kern = k_fill_tiles_smem<HK, BOUNDED, OutT, Rec32, 16>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+          (const Rec32*)A.recs, (const Rec32*)A.recs8, A.soff, A.goff8, A.perm, A.items,
+          A.n_items, A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+    } else {
+      auto kern = k_fill_tiles_smem<HK, BOUNDED, OutT, Rec, 8>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+          (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
+          A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+    }
+  } else if (A.rec_bytes == 8) {
+    k_fill_tiles_global<HK, BOUNDED, OutT, Rec32><<<grid * 2, kTileThreads, 0, st>>>(
+        (const Rec32*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
+        A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
   } else {
-    k_fill_tiles_global<HK, BOUNDED, OutT><<<grid * 2, kTileThreads, 0, st>>>(
+    k_fill_tiles_global<HK, BOUNDED, OutT, Rec><<<grid * 2, kTileThreads, 0, st>>>(
         (const Rec*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
         A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
   }

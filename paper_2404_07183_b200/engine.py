@@ -81,9 +81,9 @@ def fill_pairwise(coll: DeviceCollection, op, p, apply_root, diag, a=0.0, b=math
             ptr_items = _native.ptr(items_dev) if s0 == 0 else \
                 _native.c_vp(items_dev.data_ptr() + s0 * 32)
             _native.check(lib.pcf_fill_matrix(
-                _native.ptr(coll.recs), _native.ptr(coll.recs8), _native.ptr(coll.soff),
-                _native.ptr(coll.goff8), _native.ptr(coll.perm), M,
-                ptr_items, s1 - s0, smem, mode, _native.ptr(counter), int(op), float(p),
+                _native.ptr(coll.tile_recs), _native.ptr(coll.recsg), _native.ptr(coll.soff),
+                _native.ptr(coll.goff), _native.ptr(coll.perm), M,
+                ptr_items, s1 - s0, smem, mode, coll.rec_bytes, _native.ptr(counter), int(op), float(p),
                 int(bool(apply_root)), float(a), float(b), _native.ptr(out), out_f32, ld,
                 _native.ptr(err), st), "pcf_fill_matrix")
             if between_chunks is not None:

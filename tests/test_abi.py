@@ -43,23 +43,24 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-def plan(sizes, budget=220 * 1024, max_cols=64, max_log2g=6):
+def plan(sizes, budget=220 * 1024, max_cols=64, max_log2g=6, rec_bytes=16):
     lib = _native.load()
     sizes = np.ascontiguousarray(sizes, dtype=np.int64)
     n = ctypes.c_int64()
     smem = ctypes.c_int32()
     assert lib.pcf_plan_pairwise(_native.ptr(sizes), sizes.shape[0], budget, max_cols, max_log2g,
-                                 None, 0, ctypes.byref(n), ctypes.byref(smem)) == 0
+                                 rec_bytes, None, 0, ctypes.byref(n), ctypes.byref(smem)) == 0
     items = (_native.WorkItem * max(n.value, 1))()
     assert lib.pcf_plan_pairwise(_native.ptr(sizes), sizes.shape[0], budget, max_cols, max_log2g,
-                                 ctypes.cast(items, ctypes.c_void_p), n.value, ctypes.byref(n),
-                                 ctypes.byref(smem)) == 0
+                                 rec_bytes, ctypes.cast(items, ctypes.c_void_p), n.value,
+                                 ctypes.byref(n), ctypes.byref(smem)) == 0
     return np.frombuffer(items, dtype=np.int32).reshape(-1, 8)[: n.value].copy(), smem.value
 
 
 @pytest.mark.parametrize("dist", ["appa", "small", "huge", "one", "two"])
 @pytest.mark.parametrize("max_log2g", [0, 6])
-def test_planner_covers_upper_triangle_once(dist, max_log2g):
+@pytest.mark.parametrize("rec_bytes", [16, 8])
+def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
     rng = np.random.default_rng(1)
     sizes = {
         "appa": rng.integers(10, 1001, 700),
@@ -70,7 +71,9 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g):
     }[dist]
     sizes = np.sort(sizes)[::-1].copy()
     M = sizes.shape[0]
-    items, smem = plan(sizes, max_log2g=max_log2g)
+    items, smem = plan(sizes, max_log2g=max_log2g, rec_bytes=rec_bytes)
+    gw = 128 // rec_bytes
+    units = 512 // gw
     seen = np.zeros((M, M), dtype=np.int32)
     S = np.concatenate([[0], np.cumsum(sizes)])
     threads = 512
@@ -78,12 +81,12 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g):
         C, G = 1 << logc, 1 << log2g
         assert log2g <= max_log2g
         assert col0 > row0 and col1 <= M and nrows >= 1
-        if mode == 1:  # K1: 8-row interleaved groups, 64 quarter-warps = RG x C x G
-            assert row0 % 8 == 0 and nrows <= 16
-            RG = 2 if nrows > 8 else 1
-            assert RG * C * G == 64
-            rows_b = sum(8 * sizes[row0 + 8 * k] * 16 for k in range(RG))
-            col_b = (S[min(col0 + C, col1)] - S[col0]) * 16
+        if mode == 1:  # K1: GW-row interleaved groups, 512/GW smem-phase units = RG x C x G
+            assert row0 % gw == 0 and nrows <= 2 * gw
+            RG = 2 if nrows > gw else 1
+            assert RG * C * G == units
+            rows_b = sum(gw * sizes[row0 + gw * k] * rec_bytes for k in range(RG))
+            col_b = (S[min(col0 + C, col1)] - S[col0]) * rec_bytes + 32
             al = lambda x: (x + 127) // 128 * 128  # noqa: E731
             assert al(rows_b) + 2 * al(col_b) + 4 * 512 * 8 <= smem <= 220 * 1024
         else:  # K1g: R x C pairs x G lanes in-warp
@@ -103,7 +106,7 @@ def test_planner_rejects_unsorted():
     lib = _native.load()
     sizes = np.array([3, 5], dtype=np.int64)
     n = ctypes.c_int64()
-    assert lib.pcf_plan_pairwise(_native.ptr(sizes), 2, 1 << 16, 64, 5, None, 0,
+    assert lib.pcf_plan_pairwise(_native.ptr(sizes), 2, 1 << 16, 64, 5, 16, None, 0,
                                  ctypes.byref(n), None) == 1
     assert b"sorted" in lib.pcf_last_error()
 

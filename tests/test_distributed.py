@@ -32,10 +32,10 @@ def _plan(sizes_sorted):
     n = ctypes.c_int64()
     smem = ctypes.c_int32()
     s = np.ascontiguousarray(sizes_sorted, dtype=np.int64)
-    lib.pcf_plan_pairwise(_native.ptr(s), s.shape[0], 220 * 1024, 16, 6, None, 0,
+    lib.pcf_plan_pairwise(_native.ptr(s), s.shape[0], 220 * 1024, 16, 6, 16, None, 0,
                           ctypes.byref(n), ctypes.byref(smem))
     items = (_native.WorkItem * max(n.value, 1))()
-    lib.pcf_plan_pairwise(_native.ptr(s), s.shape[0], 220 * 1024, 16, 6,
+    lib.pcf_plan_pairwise(_native.ptr(s), s.shape[0], 220 * 1024, 16, 6, 16,
                           ctypes.cast(items, ctypes.c_void_p), n.value, ctypes.byref(n),
                           ctypes.byref(smem))
     host = np.frombuffer(items, dtype=np.int32).reshape(-1, 8)[: n.value].copy()
