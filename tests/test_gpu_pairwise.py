@@ -264,3 +264,58 @@ def test_exact_mode_bitwise_large(oracle):
     assert np.array_equal(D, ref)
     Df = np.asarray(pb.pdist(fs))
     assert rel_err(Df + np.eye(400), ref + np.eye(400)) < TOL64
+
+
+def _rank_fill(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_07183_b200 import datagen as dg
+    from paper_2404_07183_b200.collection import DeviceCollection
+    from paper_2404_07183_b200.engine import fill_pairwise, items_to_device, partition_items
+    from paper_2404_07183_b200 import parallel
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t, v, off = dg.synthetic_benchmark_packed(700, rng=dg.RngSpec(99))
+        coll = DeviceCollection(t, v, off)
+        _, host, n_smem, _, smem = coll.plan()
+        mine, my_smem = partition_items(host, n_smem, world, rank)
+        M = coll.M
+        out = torch.zeros((M, M), dtype=torch.float64, device="cuda")
+        fill_pairwise(coll, 0, 1.0, True, False, out=out,
+                      items=(items_to_device(mine, "cuda"), my_smem, mine.shape[0] - my_smem,
+                             smem))
+        cpu = out.cpu()
+        parallel.assemble_matrix(cpu, dst=0)
+        if rank == 0:
+            full, _, _ = fill_pairwise(coll, 0, 1.0, True, False)
+            q.put(bool(torch.equal(cpu, full.cpu())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_fill_bitwise_equal_single_gpu():
+    """Two ranks (sharing this GPU, gloo for the assembly) fill disjoint halves of the
+    tile queue; the assembled matrix equals the single-GPU matrix bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_fill, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    assert q.get(timeout=10)
