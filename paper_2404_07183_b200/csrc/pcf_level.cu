@@ -79,9 +79,8 @@ __global__ void __launch_bounds__(LTH)
                   const int64_t* __restrict__ src, const int32_t* __restrict__ cnt,
                   const int64_t* __restrict__ leaves, int64_t nout, int64_t ntot,
                   const int64_t* __restrict__ tile_node, const int64_t* __restrict__ tile_i,
-                  int64_t* __restrict__ tile_count,
-                  const int64_t* __restrict__ tile_off, T* __restrict__ t_out,
-                  void* __restrict__ v_out_, double* __restrict__ v2_out,
+                  int* __restrict__ tile_counter, unsigned long long* __restrict__ tile_status,
+                  T* __restrict__ t_out, void* __restrict__ v_out_, double* __restrict__ v2_out,
                   int64_t* __restrict__ off_out, int32_t* __restrict__ status) {
   using VT = typename std::conditional<K == K_MOM, double, T>::type;
   const VT* __restrict__ v = reinterpret_cast<const VT*>(v_);
@@ -94,27 +93,62 @@ __global__ void __launch_bounds__(LTH)
   VT* s_v = reinterpret_cast<VT*>(dyn);                          // [WCAP]
   double* s_v2 = reinterpret_cast<double*>(dyn + WCAP * sizeof(VT));  // [WCAP] (moments)
   T* s_t = reinterpret_cast<T*>(dyn + WCAP * sizeof(VT) + (MOM ? WCAP * sizeof(double) : 0));
-  __shared__ int64_t s_next_node, s_round_end;
+  __shared__ int64_t s_next_node, s_round_end, s_tile, s_excl;
   typedef cub::BlockScan<int, LTH> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
 
   const int tid = threadIdx.x;
-  const int64_t tile = blockIdx.x;
+  // Tiles are taken in order from an atomic counter, so every tile's predecessors are
+  // running or done -- the decoupled look-back below cannot wait on an unscheduled CTA.
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  const int64_t tile = s_tile;
   // `ntot` is a host-side upper bound (the previous level's size); the live point count
   // is the end of the last output node's input range.  Tiles past it are empty.
   ntot = off[src[nout - 1] + cnt[nout - 1]];
   const int64_t e0 = tile * (int64_t)LT;
-  if (e0 >= ntot) {
-    if (!WRITE && tid == 0) tile_count[tile] = 0;
-    return;
-  }
+  if (e0 >= ntot) return;
   const int64_t e1 = min(e0 + (int64_t)LT, ntot);
+  int64_t kept_total = 0;
+  int koff_saved = 0, rounds = 0, nseg_saved = 0;
+  bool single_round = false;
+
+  // One tile = count pass (stage + walk), look-back for the tile's output offset, emit
+  // pass (re-stage -- the tile's inputs are still in L2 -- and walk again).
+  for (int emit = 0; emit < 2; ++emit) {
+  if (emit) {
+    if (tid == 0) {
+      unsigned long long excl = 0;
+      constexpr unsigned long long AGG = 1ull << 62, PRE = 2ull << 62, VAL = (1ull << 62) - 1;
+      volatile unsigned long long* st = tile_status;
+      if (tile == 0) {
+        st[0] = PRE | (unsigned long long)kept_total;
+      } else {
+        st[tile] = AGG | (unsigned long long)kept_total;
+        for (int64_t pt = tile - 1; pt >= 0;) {
+          const unsigned long long w = st[pt];
+          if ((w >> 62) == 0) continue;  // predecessor not published yet: spin
+          excl += w & VAL;
+          if ((w >> 62) == 2) break;
+          --pt;
+        }
+        st[tile] = PRE | (excl + (unsigned long long)kept_total);
+      }
+      s_excl = (int64_t)excl;
+    }
+    __syncthreads();
+  }
+  const int64_t out_base = emit ? s_excl : 0;
   int64_t kr = tile_node[tile];
   int64_t rs = e0;
-  int64_t kept_total = 0;
-  const int64_t out_base = WRITE ? tile_off[tile] : 0;
-
+  int64_t kept_run = 0;
+  rounds = 0;
   while (rs < e1) {
+    ++rounds;
+    // a single-round tile keeps its table and staged windows from the count pass
+    const bool reuse = emit && single_round;
+    int nseg = nseg_saved;
+    if (!reuse) {
     // ---- 1. segment table for this round
     int valid = 0;
     {
@@ -166,7 +200,7 @@ __global__ void __launch_bounds__(LTH)
         }
       }
     }
-    const int nseg = __syncthreads_count(valid);
+    nseg = __syncthreads_count(valid);
     // window offsets (exclusive scan of alen + blen over the segments)
     int wlen = (tid < nseg) ? seg[tid].alen + seg[tid].blen : 0;
     int woff, wtot;
@@ -183,7 +217,6 @@ __global__ void __launch_bounds__(LTH)
       seg_pos[nseg] = (int)(s_round_end - rs);
     }
     __syncthreads();
-    const int64_t re = s_round_end;
     // ---- 2. stage the input windows (flattened over all segments; coalesced within each
     //        window, every thread busy even when the tile holds many small nodes)
     {
@@ -199,6 +232,9 @@ __global__ void __launch_bounds__(LTH)
       }
     }
     __syncthreads();
+    nseg_saved = nseg;
+    }  // !reuse
+    const int64_t re = s_round_end;
     // ---- 3. walk LPT positions per thread (twice in the write pass: count, then emit)
     const int p0 = tid * LPT;  // round-relative
     const int rlen = (int)(re - rs);
@@ -274,7 +310,18 @@ __global__ void __launch_bounds__(LTH)
           comb(i - 1, jt, pv, pv2);
         }
       };
+      // branch-free merge state for merged segments: next A / B breakpoints in registers
+      // (+inf past the end), the last A breakpoint taken (duplicate test for B)
+      const T TINF = (T)INFINITY;
+      T tai = TINF, tbj = TINF, taprev = (T)-1;
+      auto load_state = [&]() {
+        if (g.pass) return;
+        tai = i < (int)g.na ? TA(i) : TINF;
+        tbj = j < (int)g.nb ? TB(j) : TINF;
+        taprev = i > 0 ? TA(i - 1) : (T)-1;
+      };
       start((int)g.m0 + (p0 - seg_pos[sg]));
+      load_state();
       for (int q = 0; q < LPT; ++q) {
         const int p = p0 + q;
         if (p >= rlen) break;
@@ -283,6 +330,7 @@ __global__ void __launch_bounds__(LTH)
           g = seg[sg];
           bind();
           start((int)g.m0);
+          load_state();
         }
         T tt;
         VT val = pv;
@@ -296,28 +344,25 @@ __global__ void __launch_bounds__(LTH)
           kp = 1;
           ++i;
         } else {
-          const int NA = (int)g.na, NB = (int)g.nb;
-          const bool takeA = (i < NA) && (j >= NB || TA(i) <= TB(j));
-          if (takeA) {
-            tt = TA(i);
-            const int jb = j + ((j < NB && TB(j) == tt) ? 1 : 0) - 1;
-            comb(i, jb, val, val2);
-            kp = (m == 0) || (val != pv) || (MOM && val2 != pv2);
+          const bool takeA = tai <= tbj;  // A first on ties (stable merge)
+          tt = takeA ? tai : tbj;
+          const bool dup = !takeA && (taprev == tt);
+          const int ia = takeA ? i : i - 1;
+          const int ib = takeA ? j - 1 + (tbj == tt ? 1 : 0) : j;
+          comb(ia, ib, val, val2);
+          kp = !dup && ((m == 0) || (val != pv) || (MOM && val2 != pv2));
+          if (!dup) {
             pv = val;
             pv2 = val2;
-            ++i;
-          } else {
-            tt = TB(j);
-            if (i > 0 && TA(i - 1) == tt) {
-              kp = 0;  // duplicate breakpoint (A took it)
-            } else {
-              comb(i - 1, j, val, val2);
-              kp = (val != pv) || (MOM && val2 != pv2);
-              pv = val;
-              pv2 = val2;
-            }
-            ++j;
           }
+          if (takeA) taprev = tai;
+          i += takeA ? 1 : 0;
+          j += takeA ? 0 : 1;
+          // reload only the advanced cursor's next breakpoint (one selected load)
+          const bool inA = takeA ? (i < (int)g.na) : (j < (int)g.nb);
+          const T nxt = inA ? (takeA ? TA(i) : TB(j)) : TINF;
+          tai = takeA ? nxt : tai;
+          tbj = takeA ? tbj : nxt;
         }
         ++m;
         if (kp) {
@@ -334,19 +379,27 @@ __global__ void __launch_bounds__(LTH)
       }
       return nk;
     };
-    const int nkeep = walk(false, 0);
     int koff, ktot;
-    Scan(scan_tmp).ExclusiveSum(nkeep, koff, ktot);
-    if (WRITE) walk(true, out_base + kept_total + koff);
-    kept_total += ktot;
+    if (emit && single_round) {
+      koff = koff_saved;
+      ktot = (int)kept_total;
+    } else {
+      const int nkeep = walk(false, 0);
+      Scan(scan_tmp).ExclusiveSum(nkeep, koff, ktot);
+      koff_saved = koff;
+    }
+    if (emit) walk(true, out_base + kept_run + koff);
+    kept_run += ktot;
     rs = re;
     kr = s_next_node;
     __syncthreads();  // shared tables are rebuilt next round
   }
-  if (tid == 0) {
-    if (!WRITE) tile_count[tile] = kept_total;
-    else if (e1 == ntot) off_out[nout] = out_base + kept_total;
+  if (!emit) {
+    kept_total = kept_run;
+    single_round = (rounds == 1);
   }
+  }
+  if (tid == 0 && e1 == ntot) off_out[nout] = s_excl + kept_total;
 }
 
 // Merge-path partition: for every tile start (and the end of the last tile) the output
@@ -396,7 +449,7 @@ int pcf_tree_level_workspace(int64_t ntot, int64_t* bytes) {
   size_t cub_b = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cub_b, (const int64_t*)nullptr, (int64_t*)nullptr,
                                 (int64_t)(ntiles > 0 ? ntiles : 1));
-  *bytes = (int64_t)(4 * 8 * (ntiles + 1) + cub_b + 256);
+  *bytes = (int64_t)(4 * 8 * (ntiles + 1) + cub_b + 256 + 16);
   return PCF_OK;
 }
 
@@ -428,10 +481,9 @@ int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
   }
   int64_t* tile_node = (int64_t*)ws_dev;
   int64_t* tile_i = tile_node + (ntiles + 1);
-  int64_t* tile_count = tile_i + (ntiles + 1);
-  int64_t* tile_off = tile_count + (ntiles + 1);
-  void* cub_tmp = (void*)(tile_off + (ntiles + 1));
-  size_t cub_b = (size_t)(ws_bytes - 4 * 8 * (ntiles + 1));
+  unsigned long long* tile_status = (unsigned long long*)(tile_i + (ntiles + 1));
+  int* tile_counter = (int*)(tile_status + (ntiles + 1));
+  cudaMemsetAsync(tile_status, 0, (ntiles + 1) * 8 + 16, s);
   const int pg = (int)((ntiles + 1 + 255) / 256);
   const unsigned grid = (unsigned)ntiles;
 #define PCF_TL(T, K, W)                                                                       \
@@ -442,15 +494,13 @@ int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
                          dsm);                                                                \
     k_level_tiled<T, K, W><<<grid, LTH, dsm, s>>>(                                            \
         (const T*)t_dev, v_dev, v2_dev, off_dev, src_dev, cnt_dev, leaves_dev, nout, ntot,   \
-        tile_node, tile_i, tile_count, tile_off, (T*)t_out_dev, v_out_dev, v2_out_dev,        \
+        tile_node, tile_i, tile_counter, tile_status, (T*)t_out_dev, v_out_dev, v2_out_dev,   \
         off_out_dev, status_dev);                                                             \
   } while (0)
 #define PCF_TL_BOTH(T, K)                                                                     \
   do {                                                                                        \
     k_tile_part<T><<<pg, 256, 0, s>>>((const T*)t_dev, off_dev, src_dev, cnt_dev, nout, ntot, \
                                       ntiles, tile_node, tile_i);                             \
-    PCF_TL(T, K, false);                                                                      \
-    cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, tile_count, tile_off, (int64_t)ntiles, s);  \
     PCF_TL(T, K, true);                                                                       \
   } while (0)
   if (is_f32) {
