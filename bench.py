@@ -234,7 +234,7 @@ def run_ours(args):
     from paper_2404_07183_b200 import _native
     from paper_2404_07183_b200.collection import DeviceCollection, current_stream_handle
     from paper_2404_07183_b200.engine import (decode_err, item_cells, items_to_device,
-                                              new_err, partition_items)
+                                              mode_runs, new_err, partition_items)
 
     world, rank, local = dist_env()
     if world > 1:
@@ -247,9 +247,8 @@ def run_ours(args):
     t, v, off, pairs, cells = workload(M)
 
     coll = DeviceCollection(t, v, off, device=dev)
-    _, host_items, n_smem, n_glob, smem = coll.plan(exact=args.exact)
-    my_items, my_smem = partition_items(host_items, n_smem, world, rank)
-    my_glob = my_items.shape[0] - my_smem
+    _, host_items, smem = coll.plan(exact=args.exact)
+    my_items = partition_items(host_items, world, rank)
     items_dev = items_to_device(my_items, dev)
     my_cells = item_cells(my_items, coll.sizes_sorted)
     out = torch.empty((M, M), dtype=torch.float64, device=dev)
@@ -265,9 +264,8 @@ def run_ours(args):
                               _native.ptr(coll.perm), M, 0, 0.0, math.inf, _native.ptr(out), 0,
                               M, _native.ptr(err), st)
         launches = 1
-        for lo, cnt, mode in ((0, my_smem, 1), (my_smem, my_glob, 0)):
-            if cnt <= 0:
-                continue
+        for lo, hi, mode in mode_runs(my_items):
+            cnt = hi - lo
             if record and mode == 1:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -310,7 +308,7 @@ def run_ours(args):
     value = pairs * args.steps / (ms * 1e-3)
     kms = [a.elapsed_time(b) for a, b in ev_k]
     k_avg = float(np.mean(kms)) if kms else float("nan")
-    smem_cells = item_cells(my_items[:my_smem], coll.sizes_sorted)
+    smem_cells = item_cells(my_items[my_items[:, 6] == 1], coll.sizes_sorted)
     peak = fp64_peak_tflops(lib, torch, st)
     achieved = FLOPS_PER_CELL_L1 * smem_cells / (k_avg * 1e-3) / 1e12
     traffic = None
@@ -398,12 +396,12 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
         dv = host_v.to(dev, non_blocking=True)
         do = host_off.to(dev, non_blocking=True)
         _build_collection(coll, dt, dv, do, off, dev)
-        items_dev, host_items, n_smem, n_glob, smem = coll.plan(exact=args.exact)
+        items_dev, host_items, smem = coll.plan(exact=args.exact)
         if world > 1:
-            mine, ms_ = partition_items(host_items, n_smem, world, rank)
-            items = (items_to_device(mine, dev), ms_, mine.shape[0] - ms_, smem)
+            mine = partition_items(host_items, world, rank)
+            items = (items_to_device(mine, dev), mine, smem)
         else:
-            items = (items_dev, n_smem, n_glob, smem)
+            items = (items_dev, host_items, smem)
         fill_pairwise(coll, 0, 1.0, True, False, out=out, items=items)
         if world > 1:
             tdist.reduce(out, dst=0)

@@ -14,7 +14,7 @@
  * plus the whole-matrix path the GPU needs (MatrixJob.run's block loop,
  * pkg/src/pcflib/matrix.py:156-234, moved on-device): pcf_plan_pairwise + pcf_fill_matrix,
  * and the reduction path that has no boundary in the reference (reduce.py:31-63,189-238):
- * pcf_tree_level / pcf_scale_minimize / pcf_moments_level.
+ * pcf_tree_level (+ pcf_scale_flag / pcf_std_flag / pcf_compact to finalise).
  *
  * Conventions
  *  - All functions return PCF_OK (0) or an error code; pcf_last_error() gives the text.
@@ -58,7 +58,8 @@ typedef struct pcf_work_item {
   int32_t col1;      /* one past the last column */
   int32_t logC;      /* columns per streamed chunk = 1 << logC */
   int32_t log2G;     /* merge-path segments per pair = 1 << log2G */
-  int32_t smem_mode; /* 1: operands staged in shared memory, 0: read from L1/L2 */
+  int32_t smem_mode; /* 1: K1 shared-memory tiles, 2: K1r one resident long row,
+                        0: K1g one lane per pair from L1/L2 (exact mode, long rows) */
   int32_t cost_hi;   /* estimated cells / 2^20 (scheduling order only) */
 } pcf_work_item;
 
@@ -95,7 +96,12 @@ int pcf_pack_sorted32(const float* tcat_dev, const float* vcat_dev, const int64_
  * rec_bytes: 16 (float64 records, 8-row groups) or 8 (float32 records, 16-row groups).
  * max_log2G caps the merge-path split: 0 = one lane per pair everywhere, which sums every
  * entry strictly left to right exactly like the reference (bitwise for p=1 and INNER);
- * 6 = up to 64 segments per pair (fastest; same cell products, summed in G runs). */
+ * 6 = up to 64 segments per pair (fastest; same cell products, summed in G runs).
+ * Items come in one contiguous, cost-descending run per kernel, in the order
+ * K1 (smem_mode 1: 8/16-row groups + streamed columns resident in shared memory),
+ * K1r (smem_mode 2: one row resident, columns from L1/L2),
+ * K1g (smem_mode 0: rows too long for shared memory, operands from L1/L2);
+ * launch pcf_fill_matrix once per run with that run's smem_mode. */
 int pcf_plan_pairwise(const int64_t* sizes_sorted, int64_t M, int64_t smem_budget,
                       int64_t max_cols, int32_t max_log2G, int32_t rec_bytes,
                       pcf_work_item* items, int64_t cap, int64_t* n_items,
@@ -105,7 +111,8 @@ int pcf_plan_pairwise(const int64_t* sizes_sorted, int64_t M, int64_t smem_budge
 /* out_dev: M x M row-major (leading dim ld) float64 (out_is_f32=0) or float32; entries
  * (perm[p], perm[q]) and mirror are written for every pair covered by items
  * [0, n_items).  counter_dev: int32 initialised to 0.  p: Lp exponent (ignored for
- * INNER).  apply_root: r = x^(1/p) as in pdist.  b may be +inf. */
+ * INNER).  apply_root: r = x^(1/p) as in pdist.  b may be +inf.  smem_mode: the run's
+ * kernel (see pcf_plan_pairwise); smem_bytes: the planner's *smem_bytes. */
 int pcf_fill_matrix(const void* recs_dev, const void* recs8_dev, const int64_t* soff_dev,
                     const int64_t* goff8_dev, const int32_t* perm_dev,
                     int64_t M, const pcf_work_item* items_dev, int64_t n_items,
@@ -148,25 +155,14 @@ int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* o
  * DFMA (2 flops each); time it with events on `stream` for the FP64 roofline. */
 int pcf_probe_fp64(double* out_dev, int iters, int blocks_per_sm, void* stream);
 
-/* ---- reduction path (mean / std / tree_reduce; pcf_reduce.cu) ----
+/* ---- reduction path (mean / std / tree_reduce; pcf_level.cu, pcf_reduce.cu) ----
  * The reference has no kernel boundary here (reduce.py:31-63,189-238 call the Python
  * sweep directly); these entry points are the device replacement.  A tree level maps
  * nodes (SoA times/values, int64 offsets) to output nodes: output k merges input nodes
- * src[k], src[k]+1 (cnt[k]=2) or passes src[k] through (cnt[k]=1).  Candidates are
- * written in place of the input positions (st/sv/flag, ntot = input point count), then
- * pcf_compact scans the keep flags and scatters the kept points.
- * op: 0 add, 1 max, 2 min, 3 mul (value computed in float64, stored in the kind). */
+ * src[k], src[k]+1 (cnt[k]=2) or passes src[k] through (cnt[k]=1).
+ * pcf_compact: exclusive scan of keep flags (ntot candidates) + scatter of the kept points,
+ * used by the finalisation (pcf_scale_flag / pcf_std_flag). */
 int pcf_scan_workspace(int64_t ntot, int64_t* bytes);
-int pcf_level_merge(int op, int is_f32, const void* t_dev, const void* v_dev,
-                    const int64_t* off_dev, const int64_t* src_dev, const int32_t* cnt_dev,
-                    int64_t nout, int64_t ntot, void* st_dev, void* sv_dev, int32_t* flag_dev,
-                    int32_t* status_dev, void* stream);
-/* Parallel-moments (Chan) level for std: per point (mean, M2) in float64, per input node
- * leaf counts `leaves_dev` (int64). */
-int pcf_level_moments(int is_f32, const void* t_dev, const double* mu_dev, const double* m2_dev,
-                      const int64_t* off_dev, const int64_t* src_dev, const int32_t* cnt_dev,
-                      const int64_t* leaves_dev, int64_t nout, int64_t ntot, void* st_dev,
-                      double* smu_dev, double* sm2_dev, int32_t* flag_dev, void* stream);
 /* value_bytes: element size of sv/sv2 (4 or 8); sv2 may be NULL. */
 int pcf_compact(int is_f32, const void* st_dev, const void* sv_dev, const void* sv2_dev,
                 int value_bytes, const int32_t* flag_dev, int64_t ntot, const int64_t* off_in_dev,

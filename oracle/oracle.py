@@ -94,12 +94,12 @@ class Oracle:
         # the reference stores (floating)acc into a T-typed matrix: round once
         return out.astype(out_dtype), ((ei.value, ej.value) if bad else None)
 
-    def row(self, tcat, vcat, off, i, op=OP_LP, p=1.0, apply_root=True):
-        """Entries D[i, j] for j > i (O(M) memory row sample)."""
+    def row(self, tcat, vcat, off, i, op=OP_LP, p=1.0, apply_root=True, a=0.0, b=math.inf):
+        """Entries D[i, j] for j > i (O(M) memory row sample) on [a, b)."""
         M = off.shape[0] - 1
         row = np.zeros(M, dtype=np.float64)
         self.lib.pcf_oracle_row(self._p(tcat), self._p(vcat), self._p(off), M, int(i), int(op),
-                                float(p), int(apply_root), 0.0, math.inf, self._p(row))
+                                float(p), int(apply_root), float(a), float(b), self._p(row))
         return row
 
     def rows_threaded(self, tcat, vcat, off, rows, op=OP_LP, p=1.0, apply_root=True,

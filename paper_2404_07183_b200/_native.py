@@ -74,12 +74,6 @@ SIGNATURES = {
     ),
     "pcf_probe_fp64": (c_int, [c_vp, c_int, c_int, c_vp]),
     "pcf_scan_workspace": (c_int, [c_i64, c_i64p]),
-    "pcf_level_merge": (
-        c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
-                c_vp]),
-    "pcf_level_moments": (
-        c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
-                c_vp, c_vp]),
     "pcf_compact": (
         c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64,
                 c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -137,7 +137,7 @@ class DeviceCollection:
 
     # -- work plan ------------------------------------------------------------------
     def plan(self, exact=False, smem_budget=_SMEM_BUDGET, max_cols=_MAX_COLS_PER_ITEM):
-        """Tile work items (cached): (items_dev, items_host, n_smem, n_global, smem).
+        """Tile work items (cached): (items_dev, items_host, smem_bytes).
 
         exact=True restricts every pair to one lane (the reference's left-to-right
         sum, bitwise for p=1 and inner products); otherwise up to a warp per pair."""
@@ -162,9 +162,8 @@ class DeviceCollection:
                                             ctypes.byref(n), ctypes.byref(smem)),
                       "pcf_plan_pairwise")
         host = np.frombuffer(items, dtype=np.int32).reshape(-1, 8)[: n.value].copy()
-        n_smem = int((host[:, 6] == 1).sum()) if n.value else 0
         dev = torch.from_numpy(host.reshape(-1)).to(self.device)
-        res = (dev, host, n_smem, n.value - n_smem, int(smem.value))
+        res = (dev, host, int(smem.value))
         self._plans[key] = res
         return res
 

@@ -114,8 +114,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   auto al = [](int64_t x) { return (x + 127) & ~(int64_t)127; };
   auto group_recs = [&](int64_t r) { return (int64_t)GW * sizes[r]; };  // r: first row of a group
   const int T = kTileThreads;
-  std::vector<pcf_work_item> smem_items, glob_items;
-  int64_t need_max = 0;
+  std::vector<pcf_work_item> runs[3];  // by kernel: K1 (mode 1), K1r (2), K1g (0)
+  int64_t need_max = 0, k1r_need = 0;
   if (max_cols < 1) max_cols = 1 << 30;
   int64_t r0 = 0;
   while (r0 < M - 1) {
@@ -148,13 +148,22 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       rows = GW << best_logRG;
       logC = best_logC;
       logG = best_logG;
-    } else {  // rows too long to stage: operands from L1/L2, G lanes in one warp
+    } else if (al(sizes[r0] * RB) <= smem_budget) {
+      // K1r: this row alone resident in shared memory, C columns x G segments per pass;
+      // G keeps >= ~128 walk steps per lane (row length dominates long-row pairs)
+      rows = 1;
+      logG = 0;
+      while (logG < std::min(max_log2G, 5) && (sizes[r0] >> (logG + 1)) >= 128) ++logG;
+      logC = 9 - logG;
+      k1r_need = std::max(k1r_need, al(sizes[r0] * RB));
+    } else {  // rows too long for shared memory: operands from L1/L2 (K1g)
       logG = std::min(max_log2G, 5);
       const int P = T >> logG;
       rows = P <= 64 ? GW : 32;
       logC = 0;
       while ((rows << (logC + 1)) <= P) ++logC;
     }
+    const int mode = smem ? 1 : (rows == 1 ? 2 : 0);
     const int64_t Rr = std::min<int64_t>(rows, M - r0);
     const int C = 1 << logC;
     const int64_t span = std::max<int64_t>(C, (max_cols / C) * C);
@@ -168,10 +177,10 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       w.col1 = (int32_t)c1;
       w.logC = logC;
       w.log2G = logG;
-      w.smem_mode = smem ? 1 : 0;
+      w.smem_mode = mode;
       const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;
       w.cost_hi = (int32_t)std::min(2.0e9, cells / 1048576.0);
-      (smem ? smem_items : glob_items).push_back(w);
+      runs[mode == 1 ? 0 : (mode == 2 ? 1 : 2)].push_back(w);
     }
     if (smem) need_max = std::max(need_max, best_need);
     r0 += Rr;
@@ -179,18 +188,17 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   auto by_cost = [](const pcf_work_item& x, const pcf_work_item& y) {
     return x.cost_hi > y.cost_hi;
   };
-  std::stable_sort(smem_items.begin(), smem_items.end(), by_cost);
-  std::stable_sort(glob_items.begin(), glob_items.end(), by_cost);
-  const int64_t total = (int64_t)(smem_items.size() + glob_items.size());
+  for (auto& r : runs) std::stable_sort(r.begin(), r.end(), by_cost);
+  const int64_t total = (int64_t)(runs[0].size() + runs[1].size() + runs[2].size());
   *n_items = total;
-  if (smem_bytes) *smem_bytes = (int32_t)need_max;
+  if (smem_bytes) *smem_bytes = (int32_t)std::max(need_max, k1r_need);
   if (items) {
     if (cap < total) {
       set_error("pcf_plan_pairwise: capacity %lld < %lld items", (long long)cap, (long long)total);
       return PCF_ERR_ARG;
     }
-    std::copy(smem_items.begin(), smem_items.end(), items);
-    std::copy(glob_items.begin(), glob_items.end(), items + smem_items.size());
+    pcf_work_item* dst = items;
+    for (auto& r : runs) dst = std::copy(r.begin(), r.end(), dst);
   }
   return PCF_OK;
 }

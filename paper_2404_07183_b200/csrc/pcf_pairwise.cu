@@ -1,5 +1,5 @@
-// Pairwise rectangle-iteration engine: K1 (shared-memory tile kernel), K1g (global-memory
-// tiles for PCFs too long to stage), the fill_block row kernel, the pair list, the
+// Pairwise rectangle-iteration engine: K1 (shared-memory tile kernel), K1r (one long row
+// resident in shared memory), K1g (global-memory tiles for PCFs too long to stage), the fill_block row kernel, the pair list, the
 // diagonal, and K3 (sort-pack).  See DESIGN.md for layouts and rooflines.
 //
 // Reference semantics being reproduced:
@@ -328,6 +328,68 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 }
 
 // --------------------------------------------------------------------------------------
+// K1r: row-resident tiles for rows too long for K1's 8-row groups (the heavy tail of c4).
+//
+// A work item is ONE size-sorted row x a column range.  The row is loaded into shared
+// memory once per item and re-read by every pair of the item; the (shorter) columns are
+// read through L1/L2.  For a long row against shorter columns almost every step of the
+// walk advances the row cursor, so nearly all operand traffic lands in shared memory
+// instead of costing one L1 line lookup per lane per step (K1g).  Lanes: C = 512/G
+// columns x G merge-path segments, the G lanes of a pair contiguous in one warp.  Row
+// loads from lanes at unrelated positions do conflict (random bank groups); the column
+// share of the steps goes to L1.  G = 1 (exact mode) is the reference's left-to-right
+// sum, bit for bit.
+template <int HK, bool BOUNDED, typename OutT, typename RT>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_fill_rowres(const RT* __restrict__ recs, const int64_t* __restrict__ soff,
+                  const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
+                  int n_items, int* __restrict__ counter, double p, double a, double b,
+                  int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
+                  unsigned long long* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RT* rowS = reinterpret_cast<RT*>(smem_raw);
+  __shared__ int s_item;
+  const int tid = threadIdx.x;
+  int cur_row = -1;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();  // also: every lane is done with the previous row
+    const int it = s_item;
+    if (it >= n_items) break;
+    const PcfWorkItem W = items[it];
+    const int ps = W.row0;
+    const int nf = (int)(soff[ps + 1] - soff[ps]);
+    if (ps != cur_row) {  // consecutive items of the same row keep it resident
+      const RT* F = recs + soff[ps];
+      for (int x = tid; x < nf; x += kTileThreads) rowS[x] = F[x];
+      cur_row = ps;
+    }
+    __syncthreads();
+    const int C = 1 << W.logC, log2G = W.log2G;
+    const int cc = tid >> log2G;
+    const int lane = tid & ((1 << log2G) - 1);
+    for (int cb = max(W.col0, ps + 1); cb < W.col1; cb += C) {
+      const int qs = cb + cc;
+      const bool ok = qs < W.col1;
+      double acc = 0.0;
+      const RT* Gv = recs + (ok ? soff[qs] : 0);
+      int ng = 0;
+      if (ok) {
+        ng = (int)(soff[qs + 1] - soff[qs]);
+        acc = lane_walk<HK, BOUNDED, 1, 1, RT>(rowS, nf, Gv, ng, lane, log2G, p, a, b);
+      }
+      for (int o = (1 << log2G) >> 1; o >= 1; o >>= 1)
+        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+      if (ok && lane == 0) {
+        const double hl = BOUNDED ? 0.0 : hval<HK>(rowS[nf - 1].v, Gv[ng - 1].v, p);
+        finish_entry<BOUNDED, OutT>(acc, hl, p, apply_root, (int64_t)perm[ps],
+                                    (int64_t)perm[qs], out, ld, M, err);
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // Diagonal: Gram entries <f, f> (computed, pyx:104 with diag=True) or exact zeros for
 // distances (never computed; matrix.py:163).  One thread per PCF, sequential walk;
 // simultaneous jumps of f against itself take one step as in the reference.
@@ -506,7 +568,7 @@ cudaError_t launch_pack32(const float* tcat, const float* vcat, const int64_t* o
 template <int HK, bool BOUNDED, typename OutT>
 static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
   const int grid = A.num_sms;  // persistent: one CTA per SM
-  if (A.smem_mode) {
+  if (A.smem_mode == 1) {
     cudaError_t e;
     if (A.rec_bytes == 8) {
       auto kern = k_fill_tiles_smem<HK, BOUNDED, OutT, Rec32, 16>;
@@ -522,6 +584,24 @@ static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
       kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
           (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
           A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+    }
+  } else if (A.smem_mode == 2) {
+    const size_t sm = (size_t)A.smem_bytes;
+    cudaError_t e;
+    if (A.rec_bytes == 8) {
+      e = cudaFuncSetAttribute(k_fill_rowres<HK, BOUNDED, OutT, Rec32>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      k_fill_rowres<HK, BOUNDED, OutT, Rec32><<<grid, kTileThreads, sm, st>>>(
+          (const Rec32*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
+          A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+    } else {
+      e = cudaFuncSetAttribute(k_fill_rowres<HK, BOUNDED, OutT, Rec>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      k_fill_rowres<HK, BOUNDED, OutT, Rec><<<grid, kTileThreads, sm, st>>>(
+          (const Rec*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
+          A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
     }
   } else if (A.rec_bytes == 8) {
     k_fill_tiles_global<HK, BOUNDED, OutT, Rec32><<<grid * 2, kTileThreads, 0, st>>>(

@@ -43,8 +43,8 @@ def fill_pairwise(coll: DeviceCollection, op, p, apply_root, diag, a=0.0, b=math
                   out=None, err=None, items=None, chunks=1, between_chunks=None, exact=False):
     """Write the full symmetric M x M matrix into `out` (device tensor, allocated if
     None).  Diagonal: <f,f> when `diag` (Gram), exact 0 otherwise.  Returns
-    (out, err, stopped).  `items` = (items_dev, n_smem, n_global, smem_bytes) or None
-    for the collection's cached plan; `exact` selects the one-lane-per-pair plan.
+    (out, err, stopped).  `items` = (items_dev, items_host, smem_bytes) or None for the
+    collection's cached plan; `exact` selects the one-lane-per-pair plan.
     `between_chunks(frac)` is called after each of `chunks` slices of the queue has
     completed on the device; returning True stops early (cancellation)."""
     torch = _torch()
@@ -57,9 +57,9 @@ def fill_pairwise(coll: DeviceCollection, op, p, apply_root, diag, a=0.0, b=math
         if err is None:
             err = new_err(dev)
         if items is None:
-            items_dev, _, n_smem, n_glob, smem = coll.plan(exact=exact)
+            items_dev, host_items, smem = coll.plan(exact=exact)
         else:
-            items_dev, n_smem, n_glob, smem = items
+            items_dev, host_items, smem = items
         st = current_stream_handle()
         out_f32 = int(out.dtype == torch.float32)
         ld = out.stride(0)
@@ -69,9 +69,8 @@ def fill_pairwise(coll: DeviceCollection, op, p, apply_root, diag, a=0.0, b=math
             _native.ptr(err), st), "pcf_fill_diagonal")
         counter = torch.zeros(1, dtype=torch.int32, device=dev)
         segs = []
-        for base, count, mode in ((0, n_smem, 1), (n_smem, n_glob, 0)):
-            if count <= 0:
-                continue
+        for base, end, mode in mode_runs(host_items):
+            count = end - base
             k = max(1, min(int(chunks), count))
             bounds = [base + (count * i) // k for i in range(k + 1)]
             segs += [(bounds[i], bounds[i + 1], mode) for i in range(k) if bounds[i + 1] > bounds[i]]
@@ -143,26 +142,37 @@ def coll_inv_host(coll):
     return inv
 
 
-def partition_items(host_items, n_smem, world, rank):
+def mode_runs(host_items):
+    """Contiguous runs (lo, hi, smem_mode) of the plan: one kernel launch per run
+    (the planner emits K1 items, then K1r, then K1g, each run cost-sorted)."""
+    modes = np.asarray(host_items, dtype=np.int32).reshape(-1, 8)[:, 6]
+    runs, lo = [], 0
+    for i in range(1, modes.shape[0] + 1):
+        if i == modes.shape[0] or modes[i] != modes[lo]:
+            runs.append((lo, i, int(modes[lo])))
+            lo = i
+    return runs
+
+
+def partition_items(host_items, world, rank):
     """Static cost-balanced split of the work queue over `world` GPUs.
 
-    Items are cost-sorted (LPT order) within the shared-memory and global groups; each
-    group is dealt out in snake order (0..W-1, W-1..0, ...), which keeps every rank's
-    share cost-sorted and balanced to within one item.  Every pair is owned by exactly
-    one rank, so results are identical for any world size.  Returns
-    (items_host_subset, n_smem_subset)."""
+    Items are cost-sorted (LPT order) within each kernel's run; each run is dealt out in
+    snake order (0..W-1, W-1..0, ...), which keeps every rank's share cost-sorted and
+    balanced to within one item.  Every pair is owned by exactly one rank, so results
+    are identical for any world size.  Returns the rank's items (same run order)."""
     if world <= 1:
-        return host_items, n_smem
-    out, counts = [], []
-    for lo, hi in ((0, n_smem), (n_smem, host_items.shape[0])):
+        return host_items
+    out = []
+    for lo, hi, _ in mode_runs(host_items):
         idx = np.arange(lo, hi)
         k = idx - lo
         cyc = k % (2 * world)
         owner = np.where(cyc < world, cyc, 2 * world - 1 - cyc)
-        sel = host_items[idx[owner == rank]]
-        out.append(sel)
-        counts.append(sel.shape[0])
-    return np.concatenate(out, axis=0), counts[0]
+        out.append(host_items[idx[owner == rank]])
+    if not out:
+        return host_items[:0]
+    return np.concatenate(out, axis=0)
 
 
 def items_to_device(host_items, device):

@@ -57,7 +57,7 @@ def plan(sizes, budget=220 * 1024, max_cols=64, max_log2g=6, rec_bytes=16):
     return np.frombuffer(items, dtype=np.int32).reshape(-1, 8)[: n.value].copy(), smem.value
 
 
-@pytest.mark.parametrize("dist", ["appa", "small", "huge", "one", "two"])
+@pytest.mark.parametrize("dist", ["appa", "small", "huge", "beyond", "one", "two"])
 @pytest.mark.parametrize("max_log2g", [0, 6])
 @pytest.mark.parametrize("rec_bytes", [16, 8])
 def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
@@ -66,6 +66,7 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
         "appa": rng.integers(10, 1001, 700),
         "small": rng.integers(1, 30, 900),
         "huge": np.concatenate([rng.integers(2000, 12000, 20), rng.integers(10, 500, 80)]),
+        "beyond": np.concatenate([rng.integers(14000, 30000, 12), rng.integers(10, 3000, 60)]),
         "one": np.array([5]),
         "two": np.array([3, 9]),
     }[dist]
@@ -89,8 +90,12 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
             col_b = (S[min(col0 + C, col1)] - S[col0]) * rec_bytes + 32
             al = lambda x: (x + 127) // 128 * 128  # noqa: E731
             assert al(rows_b) + 2 * al(col_b) + 4 * 512 * 8 <= smem <= 220 * 1024
-        else:  # K1g: R x C pairs x G lanes in-warp
-            assert nrows * C * G <= threads and G <= 32
+        elif mode == 2:  # K1r: one resident row, C columns x G segments
+            assert nrows == 1 and C * G == threads and G <= 32
+            assert (sizes[row0] * rec_bytes + 127) // 128 * 128 <= smem <= 220 * 1024
+        else:  # K1g: R x C pairs x G lanes in-warp (rows beyond shared memory)
+            assert mode == 0 and nrows * C * G <= threads and G <= 32
+            assert sizes[row0] * rec_bytes > 220 * 1024
         for r in range(row0, row0 + nrows):
             for q in range(col0, col1):
                 if q > r:
@@ -98,8 +103,11 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
     iu = np.triu_indices(M, 1)
     assert (seen[iu] == 1).all()
     assert seen.sum() == M * (M - 1) // 2
-    smem_costs = items[items[:, 6] == 1][:, 7]
-    assert (np.diff(smem_costs) <= 0).all()  # LPT order
+    for m in (1, 2, 0):
+        costs = items[items[:, 6] == m][:, 7]
+        assert (np.diff(costs) <= 0).all()  # LPT order within each kernel's run
+    runs = [m for k, m in enumerate(items[:, 6]) if k == 0 or items[k - 1, 6] != m]
+    assert runs == [m for m in (1, 2, 0) if m in runs]  # one contiguous run per kernel
 
 
 def test_planner_rejects_unsorted():

@@ -52,7 +52,7 @@ def _worker(rank, world, port, q):
         sizes = np.diff(off)
         perm = np.argsort(-sizes, kind="stable")
         items, n_smem = _plan(sizes[perm])
-        mine, _ = engine.partition_items(items, n_smem, world, rank)
+        mine = engine.partition_items(items, world, rank)
         orc = O.Oracle()
         out = torch.zeros((M, M), dtype=torch.float64)
         owned = 0

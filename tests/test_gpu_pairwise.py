@@ -283,13 +283,12 @@ def _rank_fill(rank, world, port, q):
     try:
         t, v, off = dg.synthetic_benchmark_packed(700, rng=dg.RngSpec(99))
         coll = DeviceCollection(t, v, off)
-        _, host, n_smem, _, smem = coll.plan()
-        mine, my_smem = partition_items(host, n_smem, world, rank)
+        _, host, smem = coll.plan()
+        mine = partition_items(host, world, rank)
         M = coll.M
         out = torch.zeros((M, M), dtype=torch.float64, device="cuda")
         fill_pairwise(coll, 0, 1.0, True, False, out=out,
-                      items=(items_to_device(mine, "cuda"), my_smem, mine.shape[0] - my_smem,
-                             smem))
+                      items=(items_to_device(mine, "cuda"), mine, smem))
         cpu = out.cpu()
         parallel.assemble_matrix(cpu, dst=0)
         if rank == 0:
@@ -319,3 +318,41 @@ def test_sharded_fill_bitwise_equal_single_gpu():
         p.join(timeout=600)
         assert p.exitcode == 0
     assert q.get(timeout=10)
+
+
+@pytest.mark.parametrize("recipe,f32,bounds", [("ecc", False, (0.0, math.inf)),
+                                               ("ecc", False, (0.3, 2.5)),
+                                               ("appa", False, (0.0, math.inf)),
+                                               ("ecc", True, (0.0, math.inf))])
+def test_streamed_long_pairs(oracle, recipe, f32, bounds):
+    """K2 (mode-2 items: one pair per CTA through 1024-record windows) against the C
+    oracle, forced onto most rows by a small shared-memory budget."""
+    from paper_2404_07183_b200.collection import DeviceCollection
+    from paper_2404_07183_b200.engine import decode_err, fill_pairwise
+
+    if recipe == "ecc":
+        t, v, off = dg.pack_matrices(dg.ecc_like_collection(160, nmax_exp=3.7))
+    else:
+        t, v, off = dg.synthetic_benchmark_packed(300, rng=pb.RngSpec(5))
+    if f32:
+        t, v = t.astype(np.float32), v.astype(np.float32)
+    coll = DeviceCollection(t, v, off)
+    M = coll.M
+    dev, host, smem = coll.plan(smem_budget=48 * 1024)
+    assert (host[:, 6] == 2).sum() > 0
+    a, b = bounds
+    rows = np.unique(np.linspace(0, M - 2, 10).astype(int))
+    tol = 1e-5 if f32 else TOL64
+    for p in (1.0, 2.0):
+        out, err, _ = fill_pairwise(coll, 0, p, True, False, a=a, b=b,
+                                    items=(dev, host, smem))
+        assert decode_err(err, M) is None
+        D = out.cpu().numpy().astype(np.float64)
+        tt, vv = t.astype(np.float64), v.astype(np.float64)
+        for i in rows:
+            ref = oracle.row(tt, vv, off, i, p=p, a=a, b=b)
+            assert rel_err(D[i, i + 1:], ref[i + 1:]) < tol
+        assert np.array_equal(D, D.T)
+        out2, _, _ = fill_pairwise(coll, 0, p, True, False, a=a, b=b,
+                                   items=(dev, host, smem))
+        assert np.array_equal(out2.cpu().numpy(), out.cpu().numpy())  # deterministic

@@ -39,6 +39,7 @@ QUICK = "--quick" in sys.argv
 
 def dev_time(fn, reps=3):
     fn()
+    fn()  # second warm-up: first-call allocations and plan caching settle
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()

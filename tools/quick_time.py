@@ -17,9 +17,10 @@ coll = DeviceCollection(t, v, off)
 out = torch.empty((M, M), dtype=torch.float64, device="cuda")
 for mode in modes:
     exact = mode == "exact"
-    _, host, ns, ng, smem = coll.plan(exact=exact)
+    _, host, smem = coll.plan(exact=exact)
     g = np.bincount(host[:, 5], minlength=6)
-    print(f"[{mode}] items={len(host)} smem_items={ns} global_items={ng} smem={smem} log2G hist={g.tolist()}", flush=True)
+    m = np.bincount(host[:, 6], minlength=3)
+    print(f"[{mode}] items={len(host)} per mode(K1g,K1,K1r)={m.tolist()} smem={smem} log2G hist={g.tolist()}", flush=True)
     fill_pairwise(coll, 0, 1.0, True, False, out=out, exact=exact)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
