@@ -151,6 +151,24 @@ int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* o
                         double a, double b, double* out, int64_t ld, int64_t* err_i,
                         int64_t* err_j);
 
+/* Whole matrix from host buffers: MatrixJob.run over the compiled module
+ * (pkg/src/pcflib/matrix.py:156-234 -> pack, fill_block per row block; pyx:72-121) in one
+ * call.  tcat/vcat/off: the reference pack() layout in host memory (float64, or float32
+ * when is_f32); out: host M x M (leading dimension ld) of the same kind, written in
+ * original order (diagonal: exact 0 for LP, <f,f> for INNER when diag).  Device work runs
+ * in n_chunks cost-balanced chunks of size-sorted row blocks; each chunk's finished rows
+ * are copied to `out` on a second stream while later chunks compute (pin `out` with
+ * cudaHostRegister / cudaMallocHost for the copies to overlap).  max_log2G as in
+ * pcf_plan_pairwise.  *err_i/*err_j = -1, or the first (row-major, i < j) non-finite
+ * pair.  Compute runs on `stream` (NULL: an internal stream), copies on an internal
+ * stream joined back into it; synchronises before returning.  Device buffers are cached
+ * between calls (pcf_release_workspace frees them). */
+int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_t* off,
+                    int64_t M, int op, double p, int apply_root, int diag, double a, double b,
+                    int32_t max_log2G, int32_t n_chunks, void* out, int64_t ld, int64_t* err_i,
+                    int64_t* err_j, void* stream);
+void pcf_release_workspace(void);
+
 /* Dense FP64 FMA throughput probe: nsm*blocks_per_sm CTAs x 256 threads x 8 chains x iters
  * DFMA (2 flops each); time it with events on `stream` for the FP64 roofline. */
 int pcf_probe_fp64(double* out_dev, int iters, int blocks_per_sm, void* stream);

@@ -72,6 +72,12 @@ SIGNATURES = {
         [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_dbl, c_int, c_int, c_dbl, c_dbl, c_vp,
          c_i64, c_i64p, c_i64p],
     ),
+    "pcf_matrix_host": (
+        c_int,
+        [c_vp, c_vp, c_int, c_vp, c_i64, c_int, c_dbl, c_int, c_int, c_dbl, c_dbl, c_i32, c_i32,
+         c_vp, c_i64, c_i64p, c_i64p, c_vp],
+    ),
+    "pcf_release_workspace": (None, []),
     "pcf_probe_fp64": (c_int, [c_vp, c_int, c_int, c_vp]),
     "pcf_scan_workspace": (c_int, [c_i64, c_i64p]),
     "pcf_compact": (

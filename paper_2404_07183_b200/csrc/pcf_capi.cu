@@ -114,6 +114,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   auto al = [](int64_t x) { return (x + 127) & ~(int64_t)127; };
   auto group_recs = [&](int64_t r) { return (int64_t)GW * sizes[r]; };  // r: first row of a group
   const int T = kTileThreads;
+  constexpr int64_t kK1rMinRecs = 1024;
   std::vector<pcf_work_item> runs[3];  // by kernel: K1 (mode 1), K1r (2), K1g (0)
   int64_t need_max = 0, k1r_need = 0;
   if (max_cols < 1) max_cols = 1 << 30;
@@ -148,9 +149,11 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       rows = GW << best_logRG;
       logC = best_logC;
       logG = best_logG;
-    } else if (al(sizes[r0] * RB) <= smem_budget) {
-      // K1r: this row alone resident in shared memory, C columns x G segments per pass;
-      // G keeps >= ~128 walk steps per lane (row length dominates long-row pairs)
+    } else if (sizes[r0] >= kK1rMinRecs && al(sizes[r0] * RB) <= smem_budget) {
+      // K1r: this long row alone resident in shared memory, C columns x G segments per
+      // pass; G keeps >= ~128 walk steps per lane (row length dominates long-row pairs).
+      // Short rows that miss K1 (exact mode: G = 1 needs 64 staged columns) stay on K1g,
+      // whose 32-row passes re-use each column from L1.
       rows = 1;
       logG = 0;
       while (logG < std::min(max_log2G, 5) && (sizes[r0] >> (logG + 1)) >= 128) ++logG;
@@ -164,7 +167,10 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       while ((rows << (logC + 1)) <= P) ++logC;
     }
     const int mode = smem ? 1 : (rows == 1 ? 2 : 0);
-    const int64_t Rr = std::min<int64_t>(rows, M - r0);
+    int64_t Rr = std::min<int64_t>(rows, M - r0);
+    // rows outside K1 stop at the next group boundary so that K1 can resume on an
+    // aligned interleaved group
+    if (!smem && (r0 % GW) != 0) Rr = std::min<int64_t>(Rr, GW - r0 % GW);
     const int C = 1 << logC;
     const int64_t span = std::max<int64_t>(C, (max_cols / C) * C);
     const int64_t rows_pts = S[r0 + Rr] - S[r0];

@@ -1,0 +1,350 @@
+// Whole-matrix host-buffer entry point: the GPU replacement of MatrixJob.run over the
+// compiled kernel module (pkg/src/pcflib/matrix.py:156-234: pack once, fill every row
+// block, return the dense M x M array; _sweepkern.pack / fill_block, pyx:72-121).
+//
+// One call takes the reference's pack() layout in host memory (tcat, vcat, off) and
+// returns the dense matrix in host memory, original order.  On the device:
+//
+//   H2D (SoA + size sort + plan) -> K3 pack -> diagonal -> K1/K1r/K1g fills in CHUNKS of
+//   consecutive size-sorted row blocks  ==>  D2H of each chunk's finished rows on a
+//   second stream while the next chunk computes.
+//
+// Row s of the size-sorted order is complete once every item whose row block contains s
+// (its pairs (s, q > s)) and every item whose columns contain s (row blocks before s) has
+// run; processing row blocks in ascending order therefore finishes rows in order, and the
+// D2H of chunk k (one contiguous M-entry row per finished PCF, scattered through perm to
+// its original row) overlaps the compute of chunks k+1, ...  The 80 GB result of the 100k
+// benchmark leaves the device while the kernels run instead of after them.
+//
+// Device buffers come from a grow-only workspace kept between calls (like a caching
+// allocator); pcf_release_workspace() frees it.
+#include <stdio.h>
+#include <string.h>
+#include <algorithm>
+#include <numeric>
+#include <vector>
+#include "pcf_internal.h"
+
+namespace pcfb {
+namespace {
+
+int fail(cudaError_t e, const char* where) {
+  set_error("%s: %s", where, cudaGetErrorString(e));
+  return PCF_ERR_CUDA;
+}
+
+// grow-only device workspace, one slot per buffer role
+enum Slot { W_T, W_V, W_OFF, W_PERM, W_SOFF, W_GOFF, W_RECS, W_RECSG, W_TILE, W_ITEMS, W_CNT,
+            W_ERR, W_OUT, W_NSLOT };
+struct Workspace {
+  int device = -1;
+  void* p[W_NSLOT] = {};
+  size_t sz[W_NSLOT] = {};
+  cudaStream_t s0 = nullptr, s1 = nullptr;
+  void release() {
+    for (int k = 0; k < W_NSLOT; ++k) {
+      if (p[k]) cudaFree(p[k]);
+      p[k] = nullptr;
+      sz[k] = 0;
+    }
+    if (s0) cudaStreamDestroy(s0);
+    if (s1) cudaStreamDestroy(s1);
+    s0 = s1 = nullptr;
+    device = -1;
+  }
+  cudaError_t get(Slot k, size_t bytes, void** out) {
+    bytes = bytes ? bytes : 16;
+    if (sz[k] < bytes) {
+      if (p[k]) cudaFree(p[k]);
+      p[k] = nullptr;
+      sz[k] = 0;
+      cudaError_t e = cudaMalloc(&p[k], bytes);
+      if (e != cudaSuccess) return e;
+      sz[k] = bytes;
+    }
+    *out = p[k];
+    return cudaSuccess;
+  }
+};
+Workspace g_ws;
+
+// ld.global-style row copy list for one chunk: original row perm[s] of the device matrix
+// to the same row of the host matrix
+cudaError_t copy_rows(const std::vector<int32_t>& perm, int64_t s0, int64_t s1, const char* dsrc,
+                      char* hdst, int64_t M, int64_t ld, size_t es, cudaStream_t st) {
+  const size_t n = (size_t)(s1 - s0);
+  if (n == 0) return cudaSuccess;
+  std::vector<void*> dst(n), src(n);
+  std::vector<size_t> sizes(n, (size_t)M * es);
+  for (size_t k = 0; k < n; ++k) {
+    const int64_t o = perm[s0 + (int64_t)k];
+    src[k] = (void*)(dsrc + (size_t)o * (size_t)M * es);
+    dst[k] = (void*)(hdst + (size_t)o * (size_t)ld * es);
+  }
+  cudaMemcpyAttributes attr;
+  memset(&attr, 0, sizeof(attr));
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t attr_idx = 0, fail_idx = 0;
+  cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), n, &attr, &attr_idx,
+                                       1, &fail_idx, st);
+  if (e == cudaSuccess) return e;
+  cudaGetLastError();  // batch API unavailable (old driver): one copy per row
+  for (size_t k = 0; k < n; ++k) {
+    e = cudaMemcpyAsync(dst[k], src[k], sizes[k], cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+}  // namespace pcfb
+
+using namespace pcfb;
+
+extern "C" {
+
+void pcf_release_workspace(void) { g_ws.release(); }
+
+int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_t* off, int64_t M,
+                    int op, double p, int apply_root, int diag, double a, double b,
+                    int32_t max_log2G, int32_t n_chunks, void* out, int64_t ld, int64_t* err_i,
+                    int64_t* err_j, void* stream) {
+  if (err_i) *err_i = -1;
+  if (err_j) *err_j = -1;
+  if (!tcat || !vcat || !off || !out || M < 1 || ld < M || (op != PCF_OP_LP && op != PCF_OP_INNER) ||
+      !(a >= 0.0) || !(a < b) || M > 0x7fffffff) {
+    set_error("pcf_matrix_host: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  if (n_chunks < 1) n_chunks = 1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(e, "pcf_matrix_host device");
+  if (g_ws.device != dev) {
+    g_ws.release();
+    g_ws.device = dev;
+  }
+  if (!g_ws.s0) {
+    if ((e = cudaStreamCreateWithFlags(&g_ws.s0, cudaStreamNonBlocking)) ||
+        (e = cudaStreamCreateWithFlags(&g_ws.s1, cudaStreamNonBlocking)))
+      return fail(e, "pcf_matrix_host streams");
+  }
+  // compute on the caller's stream (events around the call then bracket all of its
+  // device work), copies on a second stream joined back into it before returning
+  cudaStream_t s0 = stream ? (cudaStream_t)stream : g_ws.s0, s1 = g_ws.s1;
+
+  // ---- host: size sort (descending, stable), sorted offsets, group offsets, plan
+  const int64_t N = off[M] - off[0];
+  std::vector<int64_t> sizes(M);
+  for (int64_t i = 0; i < M; ++i) {
+    sizes[i] = off[i + 1] - off[i];
+    if (sizes[i] < 1) {
+      set_error("pcf_matrix_host: PCF %lld has no rows", (long long)i);
+      return PCF_ERR_ARG;
+    }
+  }
+  std::vector<int32_t> perm(M);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(),
+                   [&](int32_t x, int32_t y) { return sizes[x] > sizes[y]; });
+  std::vector<int64_t> ss(M), soff(M + 1, 0);
+  for (int64_t s = 0; s < M; ++s) {
+    ss[s] = sizes[perm[s]];
+    soff[s + 1] = soff[s] + ss[s];
+  }
+  const int rec_bytes = is_f32 ? 8 : 16;
+  const int GW = 128 / rec_bytes;
+  std::vector<int64_t> goff((M + GW - 1) / GW + 1);
+  int rc = pcf_group_offsets(ss.data(), M, GW, goff.data());
+  if (rc) return rc;
+  int64_t n_items = 0;
+  int32_t smem = 0;
+  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, 2048, max_log2G, rec_bytes, nullptr, 0,
+                         &n_items, &smem);
+  if (rc) return rc;
+  std::vector<pcf_work_item> items(n_items > 0 ? n_items : 1);
+  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, 2048, max_log2G, rec_bytes, items.data(),
+                         n_items, &n_items, &smem);
+  if (rc) return rc;
+  items.resize(n_items);
+
+  // ---- chunks of consecutive row blocks, cost-balanced, at most kRowsCap rows each
+  auto item_cells = [&](const pcf_work_item& w) {
+    const double rows_pts = (double)(soff[w.row0 + w.nrows] - soff[w.row0]);
+    return (double)w.nrows * (double)(soff[w.col1] - soff[w.col0]) +
+           (double)(w.col1 - w.col0) * rows_pts;
+  };
+  std::stable_sort(items.begin(), items.end(), [](const pcf_work_item& x, const pcf_work_item& y) {
+    return x.row0 < y.row0;
+  });
+  double total = 0.0;
+  for (auto& w : items) total += item_cells(w);
+  const int64_t kRowsCap = 2048;
+  struct Chunk { int64_t i0, i1, row_end; };
+  std::vector<Chunk> chunks;
+  {
+    int64_t i = 0, start = 0, rows_start = 0;
+    double acc = 0.0;
+    while (i < n_items) {
+      const int32_t r = items[i].row0;
+      int64_t j = i;
+      double c = 0.0;
+      int64_t rend = r;
+      while (j < n_items && items[j].row0 == r) {
+        c += item_cells(items[j]);
+        rend = std::max<int64_t>(rend, (int64_t)items[j].row0 + items[j].nrows);
+        ++j;
+      }
+      acc += c;
+      i = j;
+      if (acc >= total / n_chunks || rend - rows_start >= kRowsCap || i == n_items) {
+        chunks.push_back({start, i, i == n_items ? M : rend});
+        start = i;
+        rows_start = rend;
+        acc = 0.0;
+      }
+    }
+    if (chunks.empty()) chunks.push_back({0, 0, M});
+  }
+  // inside a chunk: one run per kernel (K1, K1r, K1g), each longest-first
+  auto mode_rank = [](int m) { return m == 1 ? 0 : (m == 2 ? 1 : 2); };
+  for (auto& ch : chunks) {
+    std::stable_sort(items.begin() + ch.i0, items.begin() + ch.i1,
+                     [&](const pcf_work_item& x, const pcf_work_item& y) {
+                       const int mx = mode_rank(x.smem_mode), my = mode_rank(y.smem_mode);
+                       if (mx != my) return mx < my;
+                       return x.cost_hi > y.cost_hi;
+                     });
+  }
+
+  // ---- device buffers
+  const size_t es = is_f32 ? 4 : 8;
+  void *d_t, *d_v, *d_off, *d_perm, *d_soff, *d_goff, *d_recs, *d_recsg, *d_tile, *d_items,
+      *d_cnt, *d_err, *d_out;
+  const int64_t ng = goff.back();
+  if ((e = g_ws.get(W_T, N * es, &d_t)) || (e = g_ws.get(W_V, N * es, &d_v)) ||
+      (e = g_ws.get(W_OFF, (M + 1) * 8, &d_off)) || (e = g_ws.get(W_PERM, M * 4, &d_perm)) ||
+      (e = g_ws.get(W_SOFF, (M + 1) * 8, &d_soff)) ||
+      (e = g_ws.get(W_GOFF, goff.size() * 8, &d_goff)) ||
+      (e = g_ws.get(W_RECS, N * 16, &d_recs)) ||
+      (e = g_ws.get(W_RECSG, ng * (size_t)rec_bytes, &d_recsg)) ||
+      (e = g_ws.get(W_TILE, is_f32 ? (N + 2) * 8 : 16, &d_tile)) ||
+      (e = g_ws.get(W_ITEMS, std::max<int64_t>(n_items, 1) * sizeof(pcf_work_item), &d_items)) ||
+      (e = g_ws.get(W_CNT, 64, &d_cnt)) || (e = g_ws.get(W_ERR, 8, &d_err)) ||
+      (e = g_ws.get(W_OUT, (size_t)M * (size_t)M * es, &d_out)))
+    return fail(e, "pcf_matrix_host alloc");
+
+  // rebase offsets to 0 if the caller passed a slice
+  std::vector<int64_t> off0;
+  const int64_t* offp = off;
+  if (off[0] != 0) {
+    off0.resize(M + 1);
+    for (int64_t i = 0; i <= M; ++i) off0[i] = off[i] - off[0];
+    offp = off0.data();
+  }
+  const char* tsrc = (const char*)tcat + off[0] * es;
+  const char* vsrc = (const char*)vcat + off[0] * es;
+  if ((e = cudaMemcpyAsync(d_t, tsrc, N * es, cudaMemcpyHostToDevice, s0)) ||
+      (e = cudaMemcpyAsync(d_v, vsrc, N * es, cudaMemcpyHostToDevice, s0)) ||
+      (e = cudaMemcpyAsync(d_off, offp, (M + 1) * 8, cudaMemcpyHostToDevice, s0)) ||
+      (e = cudaMemcpyAsync(d_perm, perm.data(), M * 4, cudaMemcpyHostToDevice, s0)) ||
+      (e = cudaMemcpyAsync(d_soff, soff.data(), (M + 1) * 8, cudaMemcpyHostToDevice, s0)) ||
+      (e = cudaMemcpyAsync(d_goff, goff.data(), goff.size() * 8, cudaMemcpyHostToDevice, s0)) ||
+      (e = cudaMemcpyAsync(d_items, items.data(), n_items * sizeof(pcf_work_item),
+                           cudaMemcpyHostToDevice, s0)) ||
+      (e = cudaMemsetAsync(d_err, 0xff, 8, s0)))
+    return fail(e, "pcf_matrix_host upload");
+  // K3 pack (float64 records for the diagonal and K1r/K1g of float64; float32 collections
+  // also get the 8-byte tile records)
+  if (!is_f32) {
+    e = launch_pack(d_t, d_v, 0, (const int64_t*)d_off, (const int32_t*)d_perm,
+                    (const int64_t*)d_soff, M, d_recs, (const int64_t*)d_goff, d_recsg, s0);
+  } else {
+    e = launch_pack(d_t, d_v, 1, (const int64_t*)d_off, (const int32_t*)d_perm,
+                    (const int64_t*)d_soff, M, d_recs, nullptr, nullptr, s0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_tile, 0, (N + 2) * 8, s0);
+    if (e == cudaSuccess)
+      e = launch_pack32((const float*)d_t, (const float*)d_v, (const int64_t*)d_off,
+                        (const int32_t*)d_perm, (const int64_t*)d_soff, M, d_tile,
+                        (const int64_t*)d_goff, d_recsg, s0);
+  }
+  if (e) return fail(e, "pcf_matrix_host pack");
+  if ((e = launch_diag(d_recs, (const int64_t*)d_soff, (const int32_t*)d_perm, M, diag, a, b, d_out,
+                       is_f32, M, (unsigned long long*)d_err, s0)))
+    return fail(e, "pcf_matrix_host diagonal");
+
+  FillArgs A;
+  A.recs = is_f32 ? d_tile : d_recs;
+  A.recs8 = d_recsg;
+  A.soff = (const int64_t*)d_soff;
+  A.goff8 = (const int64_t*)d_goff;
+  A.perm = (const int32_t*)d_perm;
+  A.M = M;
+  A.counter = (int*)d_cnt;
+  A.op = op;
+  A.p = p;
+  A.a = a;
+  A.b = b;
+  A.apply_root = apply_root;
+  A.out = d_out;
+  A.out_f32 = is_f32;
+  A.ld = M;
+  A.err = (unsigned long long*)d_err;
+  A.smem_bytes = smem;
+  A.rec_bytes = rec_bytes;
+  {
+    int n = 0;
+    A.num_sms = (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+                 n > 0) ? n : 148;
+  }
+  std::vector<cudaEvent_t> evs(chunks.size(), nullptr);
+  int64_t row_done = 0;
+  int status = PCF_OK;
+  for (size_t k = 0; k < chunks.size() && status == PCF_OK; ++k) {
+    const Chunk& ch = chunks[k];
+    for (int64_t i = ch.i0; i < ch.i1;) {
+      int64_t j = i;
+      while (j < ch.i1 && items[j].smem_mode == items[i].smem_mode) ++j;
+      A.items = (const PcfWorkItem*)d_items + i;
+      A.n_items = (int)(j - i);
+      A.smem_mode = items[i].smem_mode;
+      if ((e = cudaMemsetAsync(d_cnt, 0, 4, s0)) || (e = launch_fill_tiles(A, s0))) {
+        status = fail(e, "pcf_matrix_host fill");
+        break;
+      }
+      i = j;
+    }
+    if (status) break;
+    if ((e = cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming)) ||
+        (e = cudaEventRecord(evs[k], s0)) || (e = cudaStreamWaitEvent(s1, evs[k], 0)) ||
+        (e = copy_rows(perm, row_done, ch.row_end, (const char*)d_out, (char*)out, M, ld, es, s1))) {
+      status = fail(e, "pcf_matrix_host drain");
+      break;
+    }
+    row_done = ch.row_end;
+  }
+  unsigned long long key = ~0ull;
+  cudaEvent_t join = nullptr;
+  if (status == PCF_OK) {
+    if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming)) ||
+        (e = cudaEventRecord(join, s1)) || (e = cudaStreamWaitEvent(s0, join, 0)) ||
+        (e = cudaMemcpyAsync(&key, d_err, 8, cudaMemcpyDeviceToHost, s0)) ||
+        (e = cudaStreamSynchronize(s0)))
+      status = fail(e, "pcf_matrix_host sync");
+    if (join) cudaEventDestroy(join);
+  } else {
+    cudaStreamSynchronize(s0);
+    cudaStreamSynchronize(s1);
+  }
+  for (auto ev : evs)
+    if (ev) cudaEventDestroy(ev);
+  if (status) return status;
+  if (key != ~0ull) {
+    if (err_i) *err_i = (int64_t)(key / (unsigned long long)M);
+    if (err_j) *err_j = (int64_t)(key % (unsigned long long)M);
+  }
+  return PCF_OK;
+}
+
+}  // extern "C"

@@ -200,3 +200,33 @@ def item_cells(host_items, sizes_sorted):
     ncol = np.where(valid & (c1 > c0), c1 - c0, 0)
     colsum = np.where(ncol > 0, S[c1.repeat(rmax, 1)] - S[np.minimum(c0, c1)], 0)
     return int((ncol * (sizes[r] - 1) + colsum).sum())
+
+
+def matrix_host(tcat, vcat, off, op, p, apply_root, diag, a=0.0, b=math.inf, exact=False,
+                n_chunks=32, out=None, stream=None):
+    """Whole matrix through the host-buffer C-ABI call ``pcf_matrix_host`` (MatrixJob.run
+    over the compiled module, matrix.py:156-234, in one call): host SoA in, dense host
+    M x M out (original order), device chunks drained to the host while later chunks
+    compute.  `out` may be a preallocated (pinned) numpy array or torch CPU tensor;
+    `stream`: a cudaStream_t handle for the compute (None: the library's own).
+    Returns (out, err) with err None or the first non-finite pair (i, j)."""
+    lib = _native.load()
+    tcat = np.ascontiguousarray(tcat)
+    vcat = np.ascontiguousarray(vcat)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    M = int(off.shape[0] - 1)
+    f32 = tcat.dtype == np.float32
+    if out is None:
+        out = np.empty((M, M), dtype=np.float32 if f32 else np.float64)
+    ld = out.stride(0) if hasattr(out, "stride") and callable(out.stride) else \
+        out.strides[0] // out.itemsize
+    import ctypes
+
+    ei, ej = ctypes.c_int64(-1), ctypes.c_int64(-1)
+    _native.check(lib.pcf_matrix_host(
+        _native.ptr(tcat), _native.ptr(vcat), int(f32), _native.ptr(off), M, int(op), float(p),
+        int(bool(apply_root)), int(bool(diag)), float(a), float(b), 0 if exact else 6,
+        int(n_chunks), _native.ptr(out), int(ld), ctypes.byref(ei), ctypes.byref(ej), stream),
+        "pcf_matrix_host")
+    err = None if ei.value < 0 else (int(ei.value), int(ej.value))
+    return out, err

@@ -95,7 +95,10 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
             assert (sizes[row0] * rec_bytes + 127) // 128 * 128 <= smem <= 220 * 1024
         else:  # K1g: R x C pairs x G lanes in-warp (rows beyond shared memory)
             assert mode == 0 and nrows * C * G <= threads and G <= 32
-            assert sizes[row0] * rec_bytes > 220 * 1024
+            # rows beyond shared memory, or short rows that miss K1 (K1r is for >= 1024)
+            assert sizes[row0] * rec_bytes > 220 * 1024 or sizes[row0] < 1024
+        if mode != 1 and row0 % gw:  # outside K1, blocks stop at the next group boundary
+            assert (row0 + nrows - 1) // gw == row0 // gw
         for r in range(row0, row0 + nrows):
             for q in range(col0, col1):
                 if q > r:

@@ -339,7 +339,8 @@ def test_streamed_long_pairs(oracle, recipe, f32, bounds):
     coll = DeviceCollection(t, v, off)
     M = coll.M
     dev, host, smem = coll.plan(smem_budget=48 * 1024)
-    assert (host[:, 6] == 2).sum() > 0
+    # long ECC rows go to K1r, App-A rows (< 1024 records) that miss K1 to K1g
+    assert (host[:, 6] == (2 if recipe == "ecc" else 0)).sum() > 0
     a, b = bounds
     rows = np.unique(np.linspace(0, M - 2, 10).astype(int))
     tol = 1e-5 if f32 else TOL64
@@ -356,3 +357,52 @@ def test_streamed_long_pairs(oracle, recipe, f32, bounds):
         out2, _, _ = fill_pairwise(coll, 0, p, True, False, a=a, b=b,
                                    items=(dev, host, smem))
         assert np.array_equal(out2.cpu().numpy(), out.cpu().numpy())  # deterministic
+
+
+@pytest.mark.parametrize("case", ["appa_l1", "gram64", "gram32", "ecc_l2", "bounded",
+                                  "exact_l1", "divergent", "one"])
+def test_matrix_host_equals_device_fill(case, oracle):
+    """pcf_matrix_host (host buffers in/out, chunked fill with the D2H of finished rows
+    overlapping later chunks) writes exactly the matrix of the device-resident fill: the
+    same plan, every pair computed by the same lanes, only the item order differs."""
+    from paper_2404_07183_b200.collection import DeviceCollection
+    from paper_2404_07183_b200.engine import decode_err, fill_pairwise, matrix_host
+
+    op, p, root, diag, a, b, exact = 0, 1.0, True, False, 0.0, math.inf, False
+    if case in ("appa_l1", "exact_l1", "bounded"):
+        t, v, off = dg.synthetic_benchmark_packed(700, rng=pb.RngSpec(11))
+        exact = case == "exact_l1"
+        if case == "bounded":
+            a, b, p = 0.2, 1.7, 2.0
+    elif case in ("gram64", "gram32"):
+        dt = np.float32 if case == "gram32" else np.float64
+        t, v, off = dg.pack_matrices(dg.fixed_size_collection(600, 50, dtype=dt))
+        op, p, root, diag = 1, 0.0, False, True
+    elif case == "ecc_l2":
+        t, v, off = dg.pack_matrices(dg.ecc_like_collection(150, nmax_exp=3.5))
+        p = 2.0
+    elif case == "divergent":
+        mats = [f.to_matrix() for f in pb.synthetic_benchmark(40, rng=pb.RngSpec(3))]
+        mats[17] = np.array([[0.0, 1.0], [0.5, 2.0]])  # final value 2 != 0: diverges vs all
+        t, v, off = dg.pack_matrices(mats)
+    else:
+        t, v, off = dg.pack_matrices([np.array([[0.0, 1.0], [1.0, 0.0]])])
+    M = off.shape[0] - 1
+    for n_chunks in (1, 7):
+        H, herr = matrix_host(t, v, off, op, p, root, diag, a, b, exact=exact,
+                              n_chunks=n_chunks)
+        coll = DeviceCollection(t, v, off)
+        D, err, _ = fill_pairwise(coll, op, p, root, diag, a=a, b=b, exact=exact)
+        derr = decode_err(err, M)
+        assert herr == derr
+        if case == "divergent":
+            assert herr == (0, 17)
+            continue
+        assert herr is None
+        D = D.cpu().numpy()
+        assert H.dtype == D.dtype and np.array_equal(H, D), case
+    if case in ("appa_l1", "exact_l1"):
+        ref = oracle.row(t, v, off, 5)
+        if exact:
+            assert np.array_equal(H[5, 6:], ref[6:])
+        assert rel_err(H[5, 6:], ref[6:]) < TOL64
