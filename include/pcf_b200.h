@@ -169,6 +169,34 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
                     int64_t* err_j, void* stream);
 void pcf_release_workspace(void);
 
+/* ---- user combination integrals (CombinationIntegral, combine_integrate(_timedep),
+ * integrate_single, pairwise: pkg/src/pcflib/integrate.py:51-203, matrix.py:273-283).
+ * `defs` = C definitions generated from the Python integrand (jit.py): PCF_MODE (0: h(x,y),
+ * 1: antiderivative H(x,y,t)), PCF_HAS_R, PCF_HAS_U and the __device__ functions pcf_h /
+ * pcf_H / pcf_r / pcf_u.  NVRTC compiles them with the kernel template
+ * (csrc/pcf_jit_kernels.cuh) for sm_100a with --fmad=false.
+ * pcf_jit_cubin: compile only (no GPU needed); pcf_jit_load: compile + load a module.
+ * Each entry is walked by one thread in the reference's cell order (sweep.py:67-116).
+ * Status per entry: 0 ok, 1 divergent tail, 2 non-finite.  errs_dev[2] (init UINT64_MAX):
+ * atomicMin of the row-major original-index key of the first divergent / non-finite entry. */
+int pcf_jit_cubin(const char* defs, void* cubin_out, int64_t cap, int64_t* size, char* log,
+                  int64_t logcap);
+int pcf_jit_load(const char* defs, void** module, char* log, int64_t logcap);
+void pcf_jit_release(void* module);
+/* sorted rows [r0, r1) x columns (sym: q >= s, mirrored; else all q) -> out (original order) */
+int pcf_jit_matrix(void* module, const void* recs_dev, const int64_t* soff_dev,
+                   const int32_t* perm_dev, int64_t M, int sym, double a, double b,
+                   void* out_dev, int out_f32, int64_t ld, int64_t r0, int64_t r1,
+                   unsigned long long* errs_dev, void* stream);
+/* explicit (sorted-index) pairs -> value after rounding to the kind and r, status */
+int pcf_jit_pairs(void* module, const void* recs_dev, const int64_t* soff_dev,
+                  const int64_t* pairs_dev, int64_t npairs, double a, double b, int out_f32,
+                  double* res_dev, int32_t* status_dev, void* stream);
+/* integrate_single of every (sorted) PCF with pcf_u */
+int pcf_jit_single(void* module, const void* recs_dev, const int64_t* soff_dev, int64_t M,
+                   double a, double b, int out_f32, double* res_dev, int32_t* status_dev,
+                   void* stream);
+
 /* Dense FP64 FMA throughput probe: nsm*blocks_per_sm CTAs x 256 threads x 8 chains x iters
  * DFMA (2 flops each); time it with events on `stream` for the FP64 roofline. */
 int pcf_probe_fp64(double* out_dev, int iters, int blocks_per_sm, void* stream);

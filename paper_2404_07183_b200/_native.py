@@ -78,6 +78,16 @@ SIGNATURES = {
          c_vp, c_i64, c_i64p, c_i64p, c_vp],
     ),
     "pcf_release_workspace": (None, []),
+    "pcf_jit_cubin": (c_int, [ctypes.c_char_p, c_vp, c_i64, c_i64p, ctypes.c_char_p, c_i64]),
+    "pcf_jit_load": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_vp), ctypes.c_char_p, c_i64]),
+    "pcf_jit_release": (None, [c_vp]),
+    "pcf_jit_matrix": (
+        c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_dbl, c_dbl, c_vp, c_int, c_i64, c_i64,
+                c_i64, c_vp, c_vp]),
+    "pcf_jit_pairs": (
+        c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, c_vp, c_vp, c_vp]),
+    "pcf_jit_single": (
+        c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, c_vp, c_vp, c_vp]),
     "pcf_probe_fp64": (c_int, [c_vp, c_int, c_int, c_vp]),
     "pcf_scan_workspace": (c_int, [c_i64, c_i64p]),
     "pcf_compact": (

@@ -31,6 +31,8 @@ __all__ = [
     "l2_kernel_job",
     "progress_subscribe",
     "resolve_workers",
+    "pairwise",
+    "pairwise_job",
 ]
 
 _INF = math.inf
@@ -94,8 +96,11 @@ class MatrixJob:
     handle to cancel, then ``run``."""
 
     def __init__(self, collection, *, op=OP_LP, p=1.0, apply_root=False, diag=False,
-                 a=0.0, b=_INF):
+                 a=0.0, b=_INF, integral=None):
         self._coll, self._dtype = _collection_kind(collection)
+        self._integral = integral
+        if integral is not None:  # bounds live on the integral (matrix.py:113-124)
+            a, b = integral.a, integral.b
         a = float(a)
         b = float(b)
         if math.isnan(a) or math.isinf(a) or a < 0.0 or not a < b:
@@ -106,7 +111,7 @@ class MatrixJob:
         self._diag = bool(diag)
         self._a = a
         self._b = b
-        self.symmetric = True
+        self.symmetric = True if integral is None else bool(integral.symmetric)
         self._sinks = []
         self._cancel = threading.Event()
         self.entries_computed = 0
@@ -145,6 +150,8 @@ class MatrixJob:
                     sink(frac)
             return self._cancel.is_set()
 
+        if self._integral is not None:
+            return self._run_custom(coll, report, device_output)
         out, err, stopped = fill_pairwise(
             coll, self._op, self._p, self._apply_root, self._diag, self._a, self._b,
             chunks=_PROGRESS_SLICES if self._sinks else 1,
@@ -157,6 +164,29 @@ class MatrixJob:
         self.entries_computed = M * (M + 1) // 2 if self._diag else M * (M - 1) // 2
         data = out if device_output else out.cpu().numpy()
         return PairwiseMatrix(data, True, self.entries_computed)
+
+    def _run_custom(self, coll, report, device_output):
+        """Arbitrary CombinationIntegral (matrix.py:184-196): the integrand is compiled
+        for the device (jit.py); symmetric integrals fill one triangle incl. the
+        diagonal and mirror it, asymmetric ones all M^2 entries."""
+        import torch
+
+        from .combine import _status_error, fill_custom
+
+        M = coll.M
+        out = torch.zeros((M, M), dtype=coll.out_torch_dtype, device=coll.device)
+        err, stopped = fill_custom(coll, self._integral, out,
+                                   row_chunks=_PROGRESS_SLICES if self._sinks else 1,
+                                   between=report if self._sinks else None)
+        if stopped or self._cancel.is_set():
+            raise errors.Cancelled("matrix job cancelled; partial work discarded")
+        if err is not None:
+            exc = _status_error(err[0], self._integral.H is not None)
+            exc.pair = (int(err[1]), int(err[2]))
+            raise exc
+        self.entries_computed = M * (M + 1) // 2 if self.symmetric else M * M
+        data = out if device_output else out.cpu().numpy()
+        return PairwiseMatrix(data, self.symmetric, self.entries_computed)
 
     def _divergence_error(self, pair):
         i, j = int(pair[0]), int(pair[1])
@@ -189,6 +219,17 @@ def l2_kernel(collection, workers=None, a=0.0, b=_INF, device_output=False, exac
     """Pairwise L_2 inner product (Gram) matrix over [a, b)."""
     return l2_kernel_job(collection, a=a, b=b).run(workers, device_output=device_output,
                                                    exact=exact)
+
+
+def pairwise_job(collection, integral) -> MatrixJob:
+    """Job for an arbitrary combination integral (matrix.py:273-276)."""
+    return MatrixJob(collection, integral=integral)
+
+
+def pairwise(collection, integral, workers=None, device_output=False) -> PairwiseMatrix:
+    """Pairwise integrated combination matrix under an arbitrary CombinationIntegral
+    (matrix.py:279-283); the integrand runs on the device (jit.py)."""
+    return pairwise_job(collection, integral).run(workers, device_output=device_output)
 
 
 def progress_subscribe(job: MatrixJob, sink) -> None:
