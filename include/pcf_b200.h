@@ -143,6 +143,14 @@ int pcf_pair_list(const void* recs_dev, const int64_t* soff_dev, const int64_t* 
 int pcf_integrate_pair_host(const double* ft, const double* fv, int64_t nf, const double* gt,
                             const double* gv, int64_t ng, double a, double b, int op, double p,
                             double* result);
+/* sweep.iterate_rectangles / iterate_segments (pkg/src/pcflib/sweep.py:67-116): the cells
+ * of sorted PCFs s and q (q < 0: the segments of s alone) on [a, b), in order, as
+ * cells_dev[4k..4k+3] = (l, r, v_f, v_g); *count_dev = number of cells (only the first
+ * cap are written; cap = n_s + n_q suffices).  One device thread. */
+int pcf_sweep_cells(const void* recs_dev, const int64_t* soff_dev, int64_t s, int64_t q,
+                    double a, double b, double* cells_dev, int64_t cap, int64_t* count_dev,
+                    void* stream);
+
 /* _sweepkern.fill_block (pyx:88-121) on host arrays: tcat/vcat/off = pack() output
  * (float64), out = host M x M (ld) float64, rows [r0,r1).  *err_i/*err_j = -1 or the
  * first non-finite pair. */

@@ -67,6 +67,8 @@ SIGNATURES = {
     "pcf_integrate_pair_host": (
         c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, c_dbl, c_dblp]
     ),
+    "pcf_sweep_cells": (c_int, [c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_vp, c_i64, c_vp,
+                                c_vp]),
     "pcf_fill_block_host": (
         c_int,
         [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_dbl, c_int, c_int, c_dbl, c_dbl, c_vp,

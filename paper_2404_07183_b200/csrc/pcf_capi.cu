@@ -359,6 +359,19 @@ int pcf_integrate_pair_host(const double* ft, const double* fv, int64_t nf, cons
   return PCF_OK;
 }
 
+int pcf_sweep_cells(const void* recs_dev, const int64_t* soff_dev, int64_t s, int64_t q,
+                    double a, double b, double* cells_dev, int64_t cap, int64_t* count_dev,
+                    void* stream) {
+  if (!recs_dev || !soff_dev || !cells_dev || !count_dev || s < 0 || cap < 0 || !(a >= 0.0) ||
+      !(a < b)) {
+    set_error("pcf_sweep_cells: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  cudaError_t e = launch_sweep_cells(recs_dev, soff_dev, s, q, a, b, cells_dev, cap, count_dev,
+                                     (cudaStream_t)stream);
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_sweep_cells");
+}
+
 int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* off, int64_t M,
                         int64_t r0, int64_t r1, int op, double p, int apply_root, int diag,
                         double a, double b, double* out, int64_t ld, int64_t* err_i,

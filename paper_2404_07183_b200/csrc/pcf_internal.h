@@ -63,6 +63,10 @@ cudaError_t launch_pack32(const float* tcat, const float* vcat, const int64_t* o
                           const int32_t* perm, const int64_t* soff, int64_t M, void* recs32,
                           const int64_t* goff16, void* recs32g, cudaStream_t st);
 
+cudaError_t launch_sweep_cells(const void* recs, const int64_t* soff, int64_t s, int64_t q,
+                               double a, double b, double* cells, int64_t cap, int64_t* count,
+                               cudaStream_t st);
+
 constexpr int kRedBytes = 4 * kTileThreads * 8;  // K1 segment partials + tails, 2 buffers
 
 void set_error(const char* fmt, ...);

@@ -496,6 +496,63 @@ __global__ void k_pair_list(const Rec* __restrict__ recs, const int64_t* __restr
   }
 }
 
+// Cells of one sweep, in order (sweep.py:67-116): rectangles of the minimal common
+// refinement of f and g on [a, b) (q >= 0; simultaneous jumps advance both cursors, no
+// zero-width cells, the last right edge is b), or the segments of f alone (q < 0; pieces
+// [t, t_next) while t_next < b, then [t, b)).  One thread; cells[4k..4k+3] =
+// (l, r, v_f, v_g) (v_g = 0 for segments); *count = cells written.
+__global__ void k_sweep_cells(const Rec* __restrict__ recs, const int64_t* __restrict__ soff,
+                              int64_t s, int64_t q, double a, double b, double* __restrict__ cells,
+                              int64_t cap, int64_t* __restrict__ count) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const Rec* F = recs + soff[s];
+  const int nf = (int)(soff[s + 1] - soff[s]);
+  int k = upper_bound_count(nf - 1, a, [&](int x) { return F[x].t; });
+  double t = a;
+  int64_t c = 0;
+  auto emit = [&](double l, double r, double vf, double vg) {
+    if (c < cap) {
+      cells[4 * c] = l;
+      cells[4 * c + 1] = r;
+      cells[4 * c + 2] = vf;
+      cells[4 * c + 3] = vg;
+    }
+    ++c;
+  };
+  if (q < 0) {
+    while (k + 1 < nf && F[k].t < b) {
+      emit(t, F[k].t, F[k].v, 0.0);
+      t = F[k].t;
+      ++k;
+    }
+    emit(t, b, F[k].v, 0.0);
+  } else {
+    const Rec* G = recs + soff[q];
+    const int ng = (int)(soff[q + 1] - soff[q]);
+    int m = upper_bound_count(ng - 1, a, [&](int x) { return G[x].t; });
+    for (;;) {
+      const double tnf = F[k].t, tng = G[m].t;
+      const double tn = tnf < tng ? tnf : tng;
+      if (tn >= b) {
+        emit(t, b, F[k].v, G[m].v);
+        break;
+      }
+      emit(t, tn, F[k].v, G[m].v);
+      if (tnf == tn) ++k;
+      if (tng == tn) ++m;
+      t = tn;
+    }
+  }
+  *count = c;
+}
+
+cudaError_t launch_sweep_cells(const void* recs, const int64_t* soff, int64_t s, int64_t q,
+                               double a, double b, double* cells, int64_t cap, int64_t* count,
+                               cudaStream_t st) {
+  k_sweep_cells<<<1, 32, 0, st>>>((const Rec*)recs, soff, s, q, a, b, cells, cap, count);
+  return cudaGetLastError();
+}
+
 // --------------------------------------------------------------------------------------
 // K3: device-side pack.  Original-order SoA (tcat, vcat, off) -- the reference's pack()
 // output, pyx:72-85 -- into size-sorted contiguous records and, optionally, the

@@ -29,6 +29,7 @@ from .collection import current_stream_handle, require_cuda
 from .core import Pcf
 
 __all__ = ["reduce_pair", "tree_reduce", "mean", "variance", "std", "mean_many",
+           "ReductionAccumulator",
            "DeviceLevel", "mean_packed", "std_packed"]
 
 _OPS = {"add": 0, "max": 1, "min": 2, "mul": 3}
@@ -332,3 +333,61 @@ def std(collection, ddof=1) -> Pcf:
     if len(coll) < 2:
         raise errors.InsufficientData("variance needs at least two PCFs")
     return std_packed(DeviceLevel.from_pcfs(coll), ddof, take_sqrt=True).to_pcfs()[0]
+
+
+class ReductionAccumulator:
+    """Mutable PCF state for in-place associative folds (reduce.py:66-186), held on the
+    device: ``combine(other)`` sets state <- state (op) other with reduce_pair's emission
+    rule (one pcf_tree_level launch merging the two), so the state is always minimally
+    discretised.  A fresh accumulator is the canonical zero PCF; the first combine
+    replaces it by a minimised copy of ``other`` (correct for ops without an identity at
+    0, and equal to 0 (+) f for addition).  ``capacity`` is accepted for API
+    compatibility; device buffers are sized per combine."""
+
+    def __init__(self, op, dtype=np.float64, capacity=16):
+        self.op = op
+        self._code = _op_code(op)
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.float32, np.float64):
+            raise errors.MixedPrecision(f"unsupported PCF kind {self.dtype}")
+        self._state = None  # DeviceLevel with one node, None = fresh zero PCF
+        self._fresh = True
+
+    @property
+    def size(self):
+        return 1 if self._state is None else self._state.ntot
+
+    def _as_level(self, other):
+        if isinstance(other, ReductionAccumulator):
+            if other.dtype != self.dtype:
+                raise errors.MixedPrecision(
+                    f"cannot combine {self.dtype.name} with {other.dtype.name}")
+            if other._state is not None:
+                return other._state
+            return DeviceLevel.from_pcfs([other.to_pcf()])
+        if other.dtype != self.dtype:
+            raise errors.MixedPrecision(
+                f"cannot combine {self.dtype.name} with {other.dtype.name}")
+        return DeviceLevel.from_pcfs([other])
+
+    def combine(self, other) -> None:
+        """state <- state (op) other, where other is a Pcf or another accumulator."""
+        torch = _torch()
+        lvl = self._as_level(other)
+        if self._fresh:
+            self._state = _finalize(lvl, [1.0], "scale")  # minimised copy (exact x1)
+            self._fresh = False
+            return
+        st = self._state
+        t = torch.cat([st.t[: st.ntot], lvl.t[: lvl.ntot]])
+        v = torch.cat([st.v[: st.ntot], lvl.v[: lvl.ntot]])
+        off = torch.tensor([0, st.ntot, st.ntot + lvl.ntot], dtype=torch.int64,
+                           device=t.device)
+        pair = DeviceLevel(t, v, off, 2, st.ntot + lvl.ntot, self.dtype == np.float32)
+        self._state, _ = _run_tree(pair, [2], op=self._code)
+
+    def to_pcf(self) -> Pcf:
+        """Snapshot the state as an immutable Pcf."""
+        if self._state is None:
+            return Pcf._wrap(np.zeros((1, 2), dtype=self.dtype))
+        return self._state.to_pcfs()[0]

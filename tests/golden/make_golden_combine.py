@@ -68,6 +68,32 @@ def main():
                 out[key + "_scalar"] = np.array(val)
             except (pl.errors.DivergentIntegral, pl.errors.NonFinite) as exc:
                 out[key + "_scalar_error"] = np.array(type(exc).__name__)
+    # sweeps: the cells of pairs / the pieces of single PCFs (sweep.py:67-116)
+    import operator
+
+    fsets = collections(pl)
+    sweep_pairs = [("guide", 0, 1), ("guide", 2, 3), ("rnd", 0, 5), ("rnd", 3, 3),
+                   ("rnd", 7, 11), ("rnd32", 1, 2), ("appa", 0, 9)]
+    for k, (ctag, i, j) in enumerate(sweep_pairs):
+        for bi, (a, b) in enumerate(((0.0, np.inf), (0.5, 7.25), (2.0, 3.0))):
+            cells = []
+            pl.iterate_rectangles(fsets[ctag][i], fsets[ctag][j], a, b,
+                                  lambda r: cells.append(tuple(r)))
+            out[f"sweep{k}_b{bi}_rect"] = np.array(cells, dtype=np.float64)
+            segs = []
+            pl.iterate_segments(fsets[ctag][i], a, b, lambda sg: segs.append(tuple(sg)))
+            out[f"sweep{k}_b{bi}_seg"] = np.array(segs, dtype=np.float64)
+        out[f"sweep{k}_which"] = np.array([["guide", "rnd", "rnd32", "appa"].index(ctag), i, j])
+    # accumulators: sequential folds (reduce.py:66-186)
+    for oname, op in (("add", operator.add), ("max", max), ("min", min), ("mul", operator.mul)):
+        for ctag in ("guide", "rnd", "rnd32"):
+            acc = pl.ReductionAccumulator(op, dtype=fsets[ctag][0].dtype)
+            snaps = []
+            for f in fsets[ctag][:9]:
+                acc.combine(f)
+                snaps.append(acc.to_pcf().to_matrix())
+            for n, m in enumerate(snaps):
+                out[f"acc_{oname}_{ctag}_{n}"] = m
     path = os.path.join(HERE, "reference_combine.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e6:.3f} MB")

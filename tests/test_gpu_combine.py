@@ -135,3 +135,47 @@ def test_traced_integrand_without_source(gold):
 
     D2 = np.asarray(pb.pairwise(fs, pb.CombinationIntegral(h=h2, symmetric=True)))
     assert np.array_equal(D, D2)
+
+
+CTAGS = ["guide", "rnd", "rnd32", "appa"]
+
+
+@pytest.mark.parametrize("k", range(7))
+def test_sweeps_match_reference_cells(gold, k):
+    """iterate_rectangles / iterate_segments: the device enumerates exactly the
+    reference's cells (same edges, same values, same order)."""
+    ci, i, j = (int(x) for x in gold[f"sweep{k}_which"])
+    fs = pcfs(gold, CTAGS[ci])
+    for bi, (a, b) in enumerate(((0.0, math.inf), (0.5, 7.25), (2.0, 3.0))):
+        cells = []
+        pb.iterate_rectangles(fs[i], fs[j], a, b, lambda r: cells.append(tuple(r)))
+        assert np.array_equal(np.array(cells), gold[f"sweep{k}_b{bi}_rect"])
+        assert isinstance(cells and pb.Rectangle(*cells[0]), pb.Rectangle)
+        segs = []
+        pb.iterate_segments(fs[i], a, b, lambda s: segs.append(tuple(s)))
+        assert np.array_equal(np.array(segs), gold[f"sweep{k}_b{bi}_seg"])
+    with pytest.raises(errors.InvalidBounds):
+        pb.iterate_rectangles(fs[i], fs[j], 1.0, 1.0, lambda r: None)
+
+
+@pytest.mark.parametrize("oname", ["add", "max", "min", "mul"])
+@pytest.mark.parametrize("ctag", ["guide", "rnd", "rnd32"])
+def test_reduction_accumulator_matches_reference(gold, oname, ctag):
+    import operator
+
+    op = {"add": operator.add, "max": max, "min": min, "mul": operator.mul}[oname]
+    fs = pcfs(gold, ctag)
+    acc = pb.ReductionAccumulator(op, dtype=fs[0].dtype)
+    assert acc.size == 1 and acc.to_pcf().to_matrix().tolist() == [[0.0, 0.0]]
+    for n, f in enumerate(fs[:9]):
+        acc.combine(f)
+        ref = gold[f"acc_{oname}_{ctag}_{n}"]
+        got = acc.to_pcf().to_matrix()
+        assert got.dtype == ref.dtype and np.array_equal(got, ref), (n, got, ref)
+        assert acc.size == ref.shape[0]
+    other = pb.ReductionAccumulator(op, dtype=fs[0].dtype)
+    other.combine(fs[0])
+    acc.combine(other)  # accumulator (op) accumulator
+    with pytest.raises(errors.MixedPrecision):
+        acc.combine(pb.make_pcf(np.array([[0, 1]], dtype=np.float32 if ctag != "rnd32"
+                                         else np.float64)))
