@@ -362,6 +362,12 @@ def run_ours(args):
                 "algorithmic": f"{FLOPS_PER_CELL_L1} flop/cell x {smem_cells:.4e} cells per launch",
                 "kernel_ms": k_avg,
                 "cells_per_s_per_gpu": smem_cells / (k_avg * 1e-3),
+                "traffic_note": "ncu dram read+write per launch (profiles/k1_traffic.json); "
+                                "above the 81 GB algorithmic because every 8-byte scattered "
+                                "output store costs a 32-byte sector read + write",
+                # the resource that actually binds this kernel: the SM's shared-memory
+                # data pipe (128 B/clk/SM); algorithmically one 16-byte record load/cell
+                "limiter": smem_limiter(smem_cells / (k_avg * 1e-3), clk.summary()),
             },
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -369,6 +375,24 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
+
+
+def smem_limiter(cells_per_s, clocks):
+    """Shared-memory data-pipe roofline of K1 (16 algorithmic bytes per cell against
+    128 B/clk/SM x 148 SMs at the measured SM clock) plus the ncu evidence committed
+    under profiles/."""
+    mhz = clocks.get("sm_mhz") or 1965.0
+    peak = 128.0 * 148 * mhz * 1e6
+    out = {"resource": "shared-memory data pipe (LSU wavefronts, 128 B/clk/SM)",
+           "algorithmic_bytes_per_cell": 16, "achieved_GBs": cells_per_s * 16 / 1e9,
+           "peak_GBs": peak / 1e9, "frac": cells_per_s * 16 / peak}
+    path = os.path.join(ROOT, "profiles", "k1_limiter.json")
+    if os.path.exists(path):
+        try:
+            out["ncu"] = json.load(open(path))
+        except (OSError, ValueError):
+            pass
+    return out
 
 
 def run_e2e(args, t, v, off, pairs, world, rank, dev):
