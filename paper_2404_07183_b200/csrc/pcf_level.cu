@@ -1,4 +1,4 @@
-// Tiled reduction-tree level (K5 / K7, v2): one CTA per tile of LT candidate positions.
+// Tiled reduction-tree level (K5 / K7, v3): one CTA per tile of LT candidate positions.
 //
 // A level maps input nodes to output nodes (output k merges input nodes src[k], src[k]+1,
 // or passes src[k] through when cnt[k] == 1 -- reduce.py:189-208).  Output node k's
@@ -9,15 +9,18 @@
 //      ends -- binary searches only for the two partial segments at the tile edges);
 //   2. stage every segment's A and B input windows (+1 element either side for the
 //      previous-cell value and the tie checks) in shared memory with coalesced loads;
-//   3. each thread walks LPT consecutive positions from shared memory, producing the
-//      combined value and reduce_pair's keep flag (value changed w.r.t. the previous
-//      cell; duplicate breakpoints dropped; passthrough nodes kept verbatim);
-//   4. block scan of the keep flags.
+//   3. each thread walks LPT consecutive positions from shared memory ONCE, producing
+//      the combined value and reduce_pair's keep flag (value changed w.r.t. the previous
+//      cell; duplicate breakpoints dropped; passthrough nodes kept verbatim) into
+//      registers;
+//   4. block scan of the keep counts, decoupled look-back for the tile's output offset;
+//   5. each thread stores its kept points.
 //
-// Pass 1 only counts kept points per tile; a device scan of the tile counts gives every
-// tile its output offset; pass 2 recomputes the tile (inputs are read twice, nothing
-// else round-trips through HBM) and writes the kept points plus the output node offsets.
-// HBM traffic per level ~ 3 x 16 B per point for float64 (read, read, write).
+// Single pass: every input point is read once and every output point written once
+// (HBM traffic per level = 2 x 16 B per point for float64, the algorithmic minimum).
+// Tiles whose nodes need several rounds (more than MAXSEG nodes) park their kept points
+// in a scratch region until the offset is known.  Node start offsets are stored
+// tile-relative and fixed up by k_fix_offsets.
 #define CCCL_IGNORE_DEPRECATED_API 1
 #include <cub/cub.cuh>
 #include "pcf_common.cuh"
@@ -30,7 +33,10 @@ constexpr int LTH = 256;         // threads per tile CTA
 constexpr int LPT = 8;           // positions per thread
 constexpr int LT = LTH * LPT;    // candidate positions per tile
 constexpr int MAXSEG = 64;       // node segments per round
-constexpr int WCAP = LT + 4 * MAXSEG;  // staged elements per round (both windows)
+// staged elements per round (both windows, +1 element either side, plus the 16-byte
+// granule padding of the bulk copies: U - 1 elements at each end of each window)
+template <typename T>
+__host__ __device__ constexpr int wcap() { return LT + (4 + 4 * (16 / (int)sizeof(T) - 1)) * MAXSEG; }
 
 enum { K_ADD = 0, K_MAX = 1, K_MIN = 2, K_MUL = 3, K_MOM = 4 };
 
@@ -72,8 +78,8 @@ __device__ __forceinline__ int64_t corank_g(const T* __restrict__ ta, int64_t na
   return lo;
 }
 
-template <typename T, int K, bool WRITE>
-__global__ void __launch_bounds__(LTH)
+template <typename T, int K>
+__global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
     k_level_tiled(const T* __restrict__ t, const void* __restrict__ v_,
                   const double* __restrict__ v2, const int64_t* __restrict__ off,
                   const int64_t* __restrict__ src, const int32_t* __restrict__ cnt,
@@ -81,18 +87,24 @@ __global__ void __launch_bounds__(LTH)
                   const int64_t* __restrict__ tile_node, const int64_t* __restrict__ tile_i,
                   int* __restrict__ tile_counter, unsigned long long* __restrict__ tile_status,
                   T* __restrict__ t_out, void* __restrict__ v_out_, double* __restrict__ v2_out,
-                  int64_t* __restrict__ off_out, int32_t* __restrict__ status) {
+                  int64_t* __restrict__ off_out, int32_t* __restrict__ status,
+                  int64_t* __restrict__ tile_excl, T* __restrict__ x_t, void* __restrict__ x_v_,
+                  double* __restrict__ x_v2) {
   using VT = typename std::conditional<K == K_MOM, double, T>::type;
   const VT* __restrict__ v = reinterpret_cast<const VT*>(v_);
   VT* __restrict__ v_out = reinterpret_cast<VT*>(v_out_);
+  VT* __restrict__ x_v = reinterpret_cast<VT*>(x_v_);
   constexpr bool MOM = (K == K_MOM);
 
   __shared__ Seg seg[MAXSEG];
-  __shared__ int seg_pos[MAXSEG + 1];  // tile-relative candidate start of each segment
+  __shared__ int seg_pos[MAXSEG + 1];  // round-relative candidate start of each segment
   extern __shared__ __align__(16) unsigned char dyn[];
+  constexpr int WCAP = wcap<T>();
+  constexpr int U = 16 / (int)sizeof(T);  // elements per 16-byte bulk-copy granule
   VT* s_v = reinterpret_cast<VT*>(dyn);                          // [WCAP]
   double* s_v2 = reinterpret_cast<double*>(dyn + WCAP * sizeof(VT));  // [WCAP] (moments)
   T* s_t = reinterpret_cast<T*>(dyn + WCAP * sizeof(VT) + (MOM ? WCAP * sizeof(double) : 0));
+  __shared__ uint64_t s_bar;  // bulk-copy completion of the staged windows
   __shared__ int64_t s_next_node, s_round_end, s_tile, s_excl;
   typedef cub::BlockScan<int, LTH> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -100,7 +112,12 @@ __global__ void __launch_bounds__(LTH)
   const int tid = threadIdx.x;
   // Tiles are taken in order from an atomic counter, so every tile's predecessors are
   // running or done -- the decoupled look-back below cannot wait on an unscheduled CTA.
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
+  if (tid == 0) {
+    s_tile = atomicAdd(tile_counter, 1);
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
+  uint32_t bar_phase = 0;
   __syncthreads();
   const int64_t tile = s_tile;
   // `ntot` is a host-side upper bound (the previous level's size); the live point count
@@ -109,46 +126,20 @@ __global__ void __launch_bounds__(LTH)
   const int64_t e0 = tile * (int64_t)LT;
   if (e0 >= ntot) return;
   const int64_t e1 = min(e0 + (int64_t)LT, ntot);
-  int64_t kept_total = 0;
-  int koff_saved = 0, rounds = 0, nseg_saved = 0;
-  bool single_round = false;
 
-  // One tile = count pass (stage + walk), look-back for the tile's output offset, emit
-  // pass (re-stage -- the tile's inputs are still in L2 -- and walk again).
-  for (int emit = 0; emit < 2; ++emit) {
-  if (emit) {
-    if (tid == 0) {
-      unsigned long long excl = 0;
-      constexpr unsigned long long AGG = 1ull << 62, PRE = 2ull << 62, VAL = (1ull << 62) - 1;
-      volatile unsigned long long* st = tile_status;
-      if (tile == 0) {
-        st[0] = PRE | (unsigned long long)kept_total;
-      } else {
-        st[tile] = AGG | (unsigned long long)kept_total;
-        for (int64_t pt = tile - 1; pt >= 0;) {
-          const unsigned long long w = st[pt];
-          if ((w >> 62) == 0) continue;  // predecessor not published yet: spin
-          excl += w & VAL;
-          if ((w >> 62) == 2) break;
-          --pt;
-        }
-        st[tile] = PRE | (excl + (unsigned long long)kept_total);
-      }
-      s_excl = (int64_t)excl;
-    }
-    __syncthreads();
-  }
-  const int64_t out_base = emit ? s_excl : 0;
+  // this thread's kept outputs of a single-round tile stay in registers until the
+  // tile's output offset is known
+  T o_t[LPT];
+  VT o_v[LPT];
+  double o_v2[LPT];
+  int my_koff = 0;
+  unsigned my_kmask = 0;
+  bool multi = false;
+
   int64_t kr = tile_node[tile];
   int64_t rs = e0;
-  int64_t kept_run = 0;
-  rounds = 0;
+  int kept_run = 0;
   while (rs < e1) {
-    ++rounds;
-    // a single-round tile keeps its table and staged windows from the count pass
-    const bool reuse = emit && single_round;
-    int nseg = nseg_saved;
-    if (!reuse) {
     // ---- 1. segment table for this round
     int valid = 0;
     {
@@ -170,8 +161,6 @@ __global__ void __launch_bounds__(LTH)
           g.m0 = ss - b;
           g.m1 = se - b;
           g.pass = (c == 1);
-          const T* ta = t + b;
-          const T* tb = t + b + la;
           if (g.pass) {
             g.i0 = g.m0; g.j0 = 0; g.i1 = g.m1; g.j1 = 0;
           } else {
@@ -200,14 +189,22 @@ __global__ void __launch_bounds__(LTH)
         }
       }
     }
-    nseg = __syncthreads_count(valid);
-    // window offsets (exclusive scan of alen + blen over the segments)
-    int wlen = (tid < nseg) ? seg[tid].alen + seg[tid].blen : 0;
-    int woff, wtot;
-    Scan(scan_tmp).ExclusiveSum(wlen, woff, wtot);
+    const int nseg = __syncthreads_count(valid);
+    // window offsets: each window padded out to whole 16-byte granules of the global
+    // arrays (exclusive scan of the padded lengths keeps every window granule-aligned)
+    int la_p = 0, lb_p = 0;
     if (tid < nseg) {
-      seg[tid].aoff = woff;
-      seg[tid].boff = woff + seg[tid].alen;
+      const Seg& g = seg[tid];
+      la_p = (int)(((g.ga + g.alen + U - 1) & ~(int64_t)(U - 1)) - (g.ga & ~(int64_t)(U - 1)));
+      lb_p = g.blen > 0 ? (int)(((g.gb + g.blen + U - 1) & ~(int64_t)(U - 1)) -
+                                (g.gb & ~(int64_t)(U - 1)))
+                        : 0;
+    }
+    int woff, wtot;
+    Scan(scan_tmp).ExclusiveSum(la_p + lb_p, woff, wtot);
+    if (tid < nseg) {
+      seg[tid].aoff = woff + (int)(seg[tid].ga & (U - 1));
+      seg[tid].boff = woff + la_p + (int)(seg[tid].gb & (U - 1));
       seg_pos[tid] = (int)(seg[tid].base + seg[tid].m0 - rs);
     }
     if (tid == 0) {
@@ -216,31 +213,54 @@ __global__ void __launch_bounds__(LTH)
       s_next_node = kr + nseg;
       seg_pos[nseg] = (int)(s_round_end - rs);
     }
-    __syncthreads();
-    // ---- 2. stage the input windows (flattened over all segments; coalesced within each
-    //        window, every thread busy even when the tile holds many small nodes)
-    {
-      int sgw = 0;
-#pragma unroll 2
-      for (int w = tid; w < wtot; w += LTH) {
-        while (sgw + 1 < nseg && seg[sgw + 1].aoff <= w) ++sgw;  // w increases per thread
-        const int boff = seg[sgw].boff;
-        const int64_t gi = (w < boff) ? seg[sgw].ga + (w - seg[sgw].aoff) : seg[sgw].gb + (w - boff);
-        s_t[w] = t[gi];
-        s_v[w] = v[gi];
-        if (MOM) s_v2[w] = v2[gi];
+    // ---- 2. stage the input windows with TMA bulk copies (one issuing thread per
+    //        segment; whole granules up to the last one, which may end past the array and
+    //        is loaded element-wise instead)
+    if (tid < nseg) {
+      const Seg g = seg[tid];
+      fence_proxy_async();
+      uint32_t bytes = 0;
+      int64_t lo_[2], hi_[2];
+      int dst_[2];
+      lo_[0] = g.ga & ~(int64_t)(U - 1);
+      hi_[0] = (g.ga + g.alen) & ~(int64_t)(U - 1);
+      dst_[0] = woff;
+      lo_[1] = g.gb & ~(int64_t)(U - 1);
+      hi_[1] = g.blen > 0 ? ((g.gb + g.blen) & ~(int64_t)(U - 1)) : lo_[1];
+      dst_[1] = woff + la_p;
+      for (int w = 0; w < 2; ++w)
+        if (hi_[w] > lo_[w])
+          bytes += (uint32_t)((hi_[w] - lo_[w]) * (sizeof(T) + sizeof(VT) + (MOM ? 8 : 0)));
+      if (bytes) mbar_expect_tx(&s_bar, bytes);
+      for (int w = 0; w < 2; ++w) {
+        if (hi_[w] > lo_[w]) {
+          const uint32_t n = (uint32_t)(hi_[w] - lo_[w]);
+          bulk_g2s(s_t + dst_[w], t + lo_[w], n * (uint32_t)sizeof(T), &s_bar);
+          bulk_g2s(s_v + dst_[w], v + lo_[w], n * (uint32_t)sizeof(VT), &s_bar);
+          if (MOM) bulk_g2s(s_v2 + dst_[w], v2 + lo_[w], n * 8u, &s_bar);
+        }
+        // the partial last granule, element-wise
+        const int64_t e = w == 0 ? g.ga + g.alen : (g.blen > 0 ? g.gb + g.blen : 0);
+        for (int64_t x = max(hi_[w], lo_[w]); x < e; ++x) {
+          const int d = dst_[w] + (int)(x - lo_[w]);
+          s_t[d] = t[x];
+          s_v[d] = v[x];
+          if (MOM) s_v2[d] = v2[x];
+        }
       }
     }
-    __syncthreads();
-    nseg_saved = nseg;
-    }  // !reuse
+    __syncthreads();  // every expect_tx is registered before the single arrival
+    if (tid == 0) mbar_arrive(&s_bar);
     const int64_t re = s_round_end;
-    // ---- 3. walk LPT positions per thread (twice in the write pass: count, then emit)
+    if (rs == e0 && re < e1) multi = true;  // the tile needs more than one round
+    mbar_wait(&s_bar, bar_phase);
+    bar_phase ^= 1u;
+    __syncthreads();  // element-wise tails visible
+    // ---- 3. walk LPT positions per thread, once: values + keep flags into registers
     const int p0 = tid * LPT;  // round-relative
     const int rlen = (int)(re - rs);
-    auto walk = [&](bool emit, int64_t pos) -> int {
-      int nk = 0;
-      if (p0 >= rlen) return 0;
+    unsigned kmask = 0, nsmask = 0;
+    if (p0 < rlen) {
       int sg;
       {
         int lo = 0, hi = nseg - 1;
@@ -322,84 +342,171 @@ __global__ void __launch_bounds__(LTH)
       };
       start((int)g.m0 + (p0 - seg_pos[sg]));
       load_state();
+#pragma unroll
       for (int q = 0; q < LPT; ++q) {
         const int p = p0 + q;
-        if (p >= rlen) break;
-        if (sg + 1 < nseg && p >= seg_pos[sg + 1]) {
-          ++sg;
-          g = seg[sg];
-          bind();
-          start((int)g.m0);
-          load_state();
-        }
-        T tt;
-        VT val = pv;
-        double val2 = pv2;
-        int kp;
-        if (emit && m == 0) off_out[g.node] = pos;  // node start: first candidate, always kept
-        if (g.pass) {
-          tt = TA(i);
-          val = VA(i);
-          if (MOM) val2 = V2A(i);
-          kp = 1;
-          ++i;
-        } else {
-          const bool takeA = tai <= tbj;  // A first on ties (stable merge)
-          tt = takeA ? tai : tbj;
-          const bool dup = !takeA && (taprev == tt);
-          const int ia = takeA ? i : i - 1;
-          const int ib = takeA ? j - 1 + (tbj == tt ? 1 : 0) : j;
-          comb(ia, ib, val, val2);
-          kp = !dup && ((m == 0) || (val != pv) || (MOM && val2 != pv2));
-          if (!dup) {
-            pv = val;
-            pv2 = val2;
+        if (p < rlen) {
+          if (sg + 1 < nseg && p >= seg_pos[sg + 1]) {
+            ++sg;
+            g = seg[sg];
+            bind();
+            start((int)g.m0);
+            load_state();
           }
-          if (takeA) taprev = tai;
-          i += takeA ? 1 : 0;
-          j += takeA ? 0 : 1;
-          // reload only the advanced cursor's next breakpoint (one selected load)
-          const bool inA = takeA ? (i < (int)g.na) : (j < (int)g.nb);
-          const T nxt = inA ? (takeA ? TA(i) : TB(j)) : TINF;
-          tai = takeA ? nxt : tai;
-          tbj = takeA ? tbj : nxt;
-        }
-        ++m;
-        if (kp) {
-          if (emit) {
-            t_out[pos] = tt;
-            v_out[pos] = val;
-            if (MOM) v2_out[pos] = val2;
-            ++pos;
-          } else if (!MOM && !isfinite((double)val)) {
-            atomicOr(status, 1);
+          T tt;
+          VT val = pv;
+          double val2 = pv2;
+          int kp;
+          if (m == 0) nsmask |= 1u << q;  // node start: first candidate, always kept
+          if (g.pass) {
+            tt = TA(i);
+            val = VA(i);
+            if (MOM) val2 = V2A(i);
+            kp = 1;
+            ++i;
+          } else {
+            const bool takeA = tai <= tbj;  // A first on ties (stable merge)
+            tt = takeA ? tai : tbj;
+            const bool dup = !takeA && (taprev == tt);
+            const int ia = takeA ? i : i - 1;
+            const int ib = takeA ? j - 1 + (tbj == tt ? 1 : 0) : j;
+            comb(ia, ib, val, val2);
+            kp = !dup && ((m == 0) || (val != pv) || (MOM && val2 != pv2));
+            if (!dup) {
+              pv = val;
+              pv2 = val2;
+            }
+            if (takeA) taprev = tai;
+            i += takeA ? 1 : 0;
+            j += takeA ? 0 : 1;
+            // reload only the advanced cursor's next breakpoint (one selected load)
+            const bool inA = takeA ? (i < (int)g.na) : (j < (int)g.nb);
+            const T nxt = inA ? (takeA ? TA(i) : TB(j)) : TINF;
+            tai = takeA ? nxt : tai;
+            tbj = takeA ? tbj : nxt;
           }
-          ++nk;
+          ++m;
+          o_t[q] = tt;
+          o_v[q] = val;
+          o_v2[q] = val2;
+          if (kp) {
+            kmask |= 1u << q;
+            if (!MOM && !isfinite((double)val)) atomicOr(status, 1);
+          }
         }
       }
-      return nk;
-    };
-    int koff, ktot;
-    if (emit && single_round) {
-      koff = koff_saved;
-      ktot = (int)kept_total;
-    } else {
-      const int nkeep = walk(false, 0);
-      Scan(scan_tmp).ExclusiveSum(nkeep, koff, ktot);
-      koff_saved = koff;
     }
-    if (emit) walk(true, out_base + kept_run + koff);
+    const int nk = __popc(kmask);
+    int koff, ktot;
+    Scan(scan_tmp).ExclusiveSum(nk, koff, ktot);
+    // node starts of this round: tile-local output index now, the tile's offset is added
+    // by k_fix_offsets after the level (tile_excl)
+    if (nsmask) {
+      int r = 0;
+#pragma unroll
+      for (int q = 0; q < LPT; ++q) {
+        if ((kmask >> q) & 1u) {
+          if ((nsmask >> q) & 1u) {
+            const int p = p0 + q;
+            int lo = 0, hi = nseg - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (seg_pos[mid] <= p) lo = mid;
+              else hi = mid - 1;
+            }
+            off_out[seg[lo].node] = kept_run + koff + r;
+          }
+          ++r;
+        }
+      }
+    }
+    if (multi) {  // park this round's kept points in the tile's scratch region
+      int r = 0;
+#pragma unroll
+      for (int q = 0; q < LPT; ++q) {
+        if ((kmask >> q) & 1u) {
+          const int64_t x = e0 + kept_run + koff + r;
+          x_t[x] = o_t[q];
+          x_v[x] = o_v[q];
+          if (MOM) x_v2[x] = o_v2[q];
+          ++r;
+        }
+      }
+    } else {
+      my_koff = koff;
+      my_kmask = kmask;
+    }
     kept_run += ktot;
     rs = re;
     kr = s_next_node;
     __syncthreads();  // shared tables are rebuilt next round
   }
-  if (!emit) {
-    kept_total = kept_run;
-    single_round = (rounds == 1);
+  // ---- 4. decoupled look-back: the tile's output offset.  One warp inspects 32
+  //        predecessors per step (one L2 round trip), sums their aggregates back to the
+  //        nearest inclusive prefix, and publishes this tile's inclusive prefix.
+  if (tid < 32) {
+    constexpr unsigned long long AGG = 1ull << 62, PRE = 2ull << 62, VAL = (1ull << 62) - 1;
+    volatile unsigned long long* st = tile_status;
+    const int lane = tid;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st[0] = PRE | (unsigned long long)kept_run;
+    } else {
+      if (lane == 0) st[tile] = AGG | (unsigned long long)kept_run;
+      for (int64_t base = tile - 1;; base -= 32) {
+        const int64_t pt = base - lane;
+        unsigned long long w = pt >= 0 ? st[pt] : PRE;  // before tile 0: prefix 0
+        while (__any_sync(0xffffffffu, (w >> 62) == 0)) {
+          if ((w >> 62) == 0) w = st[pt];  // predecessor not published yet: spin
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+        const int first = pre ? __ffs(pre) - 1 : 32;  // nearest inclusive prefix
+        unsigned long long val = lane <= first ? (w & VAL) : 0ull;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        excl += val;
+        if (pre) break;
+      }
+      if (lane == 0) st[tile] = PRE | (excl + (unsigned long long)kept_run);
+    }
+    if (lane == 0) s_excl = (int64_t)excl;
   }
+  __syncthreads();
+  const int64_t out_base = s_excl;
+  // ---- 5. write the kept points
+  if (!multi) {
+    int r = 0;
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      if ((my_kmask >> q) & 1u) {
+        const int64_t x = out_base + my_koff + r;
+        t_out[x] = o_t[q];
+        v_out[x] = o_v[q];
+        if (MOM) v2_out[x] = o_v2[q];
+        ++r;
+      }
+    }
+  } else {
+    for (int x = tid; x < kept_run; x += LTH) {
+      t_out[out_base + x] = x_t[e0 + x];
+      v_out[out_base + x] = x_v[e0 + x];
+      if (MOM) v2_out[out_base + x] = x_v2[e0 + x];
+    }
   }
-  if (tid == 0 && e1 == ntot) off_out[nout] = s_excl + kept_total;
+  if (tid == 0) {
+    tile_excl[tile] = out_base;
+    if (e1 == ntot) off_out[nout] = out_base + kept_run;
+  }
+}
+
+// Output node offsets: node k starts in the tile holding its first candidate
+// (off[src[k]]); the level kernel stored the tile-local index, add the tile's offset.
+__global__ void k_fix_offsets(const int64_t* __restrict__ off, const int64_t* __restrict__ src,
+                              int64_t nout, const int64_t* __restrict__ tile_excl,
+                              int64_t* __restrict__ off_out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nout;
+       k += (int64_t)gridDim.x * blockDim.x)
+    off_out[k] += tile_excl[off[src[k]] / LT];
 }
 
 // Merge-path partition: for every tile start (and the end of the last tile) the output
@@ -445,11 +552,10 @@ using namespace pcfb::lvl;
 extern "C" {
 
 int pcf_tree_level_workspace(int64_t ntot, int64_t* bytes) {
+  // tile_node, tile_i, tile_status (+counter), tile_excl: ntiles+1 words each; scratch for
+  // multi-round tiles: t, v, v2 (8 bytes each) per candidate
   const int64_t ntiles = (ntot + LT - 1) / LT;
-  size_t cub_b = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, cub_b, (const int64_t*)nullptr, (int64_t*)nullptr,
-                                (int64_t)(ntiles > 0 ? ntiles : 1));
-  *bytes = (int64_t)(4 * 8 * (ntiles + 1) + cub_b + 256 + 16);
+  *bytes = (int64_t)(4 * 8 * (ntiles + 2) + 64 + 3 * 8 * (ntot > 0 ? ntot : 1) + 256);
   return PCF_OK;
 }
 
@@ -483,25 +589,33 @@ int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
   int64_t* tile_i = tile_node + (ntiles + 1);
   unsigned long long* tile_status = (unsigned long long*)(tile_i + (ntiles + 1));
   int* tile_counter = (int*)(tile_status + (ntiles + 1));
+  int64_t* tile_excl = (int64_t*)(tile_status + (ntiles + 2));
+  char* xbase = (char*)(tile_excl + (ntiles + 2));
+  xbase = (char*)(((uintptr_t)xbase + 255) & ~(uintptr_t)255);
+  void* x_t = xbase;
+  void* x_v = xbase + 8 * ntot;
+  double* x_v2 = (double*)(xbase + 16 * ntot);
   cudaMemsetAsync(tile_status, 0, (ntiles + 1) * 8 + 16, s);
   const int pg = (int)((ntiles + 1 + 255) / 256);
   const unsigned grid = (unsigned)ntiles;
-#define PCF_TL(T, K, W)                                                                       \
+#define PCF_TL(T, K)                                                                          \
   do {                                                                                        \
     typedef typename std::conditional<K == K_MOM, double, T>::type VT_;                      \
-    const int dsm = WCAP * (int)(sizeof(VT_) + sizeof(T) + (K == K_MOM ? sizeof(double) : 0)); \
-    cudaFuncSetAttribute(k_level_tiled<T, K, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+    const int dsm = wcap<T>() * (int)(sizeof(VT_) + sizeof(T) + (K == K_MOM ? sizeof(double) : 0)); \
+    cudaFuncSetAttribute(k_level_tiled<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                          dsm);                                                                \
-    k_level_tiled<T, K, W><<<grid, LTH, dsm, s>>>(                                            \
+    k_level_tiled<T, K><<<grid, LTH, dsm, s>>>(                                               \
         (const T*)t_dev, v_dev, v2_dev, off_dev, src_dev, cnt_dev, leaves_dev, nout, ntot,   \
         tile_node, tile_i, tile_counter, tile_status, (T*)t_out_dev, v_out_dev, v2_out_dev,   \
-        off_out_dev, status_dev);                                                             \
+        off_out_dev, status_dev, tile_excl, (T*)x_t, x_v, x_v2);                              \
   } while (0)
 #define PCF_TL_BOTH(T, K)                                                                     \
   do {                                                                                        \
     k_tile_part<T><<<pg, 256, 0, s>>>((const T*)t_dev, off_dev, src_dev, cnt_dev, nout, ntot, \
                                       ntiles, tile_node, tile_i);                             \
-    PCF_TL(T, K, true);                                                                       \
+    PCF_TL(T, K);                                                                             \
+    k_fix_offsets<<<(unsigned)((nout + 255) / 256 < 4096 ? (nout + 255) / 256 : 4096), 256,   \
+                    0, s>>>(off_dev, src_dev, nout, tile_excl, off_out_dev);                  \
   } while (0)
   if (is_f32) {
     switch (kind) {

@@ -153,6 +153,34 @@ def _plan_levels(seg_nodes, leaves0=None, moments=False):
     return plan, leaves
 
 
+_PLAN_CACHE = {}
+
+
+def _device_plan(seg_nodes, leaves0, moments, dev):
+    """Host pairing plan + one device upload of every level's src / cnt (/ leaves),
+    cached per tree shape (the plan depends only on the fibre sizes)."""
+    torch = _torch()
+    seg_nodes = np.asarray(seg_nodes, dtype=np.int64)
+    key = None
+    if leaves0 is None and seg_nodes.size <= 64:
+        key = (tuple(int(x) for x in seg_nodes), bool(moments), str(dev))
+        if key in _PLAN_CACHE:
+            return _PLAN_CACHE[key]
+    plan, leaves_final = _plan_levels(seg_nodes, leaves0, moments)
+    src_d = cnt_d = lv_d = None
+    if plan:
+        src_d = torch.from_numpy(np.concatenate([p[0] for p in plan])).to(dev)
+        cnt_d = torch.from_numpy(np.concatenate([p[1] for p in plan])).to(dev)
+        if moments:
+            lv_d = torch.from_numpy(np.concatenate([p[2] for p in plan])).to(dev)
+    res = (plan, leaves_final, src_d, cnt_d, lv_d)
+    if key is not None:
+        if len(_PLAN_CACHE) > 16:
+            _PLAN_CACHE.clear()
+        _PLAN_CACHE[key] = res
+    return res
+
+
 def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=None):
     """Reduce each fibre (seg_nodes[i] consecutive nodes) to one node: one tiled
     two-pass level kernel per tree level (pcf_tree_level).  The whole pairing plan is
@@ -163,17 +191,9 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
     dev = level.t.device
     st = current_stream_handle()
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    plan, leaves_final = _plan_levels(seg_nodes, leaves0, moments)
+    plan, leaves_final, src_d, cnt_d, lv_d = _device_plan(seg_nodes, leaves0, moments, dev)
     if not plan:
         return level, leaves_final
-    # one upload for every level's src / cnt (/ leaves)
-    src_all = np.concatenate([p[0] for p in plan])
-    cnt_all = np.concatenate([p[1] for p in plan])
-    src_d = torch.from_numpy(src_all).to(dev)
-    cnt_d = torch.from_numpy(cnt_all).to(dev)
-    if moments:
-        lv_all = np.concatenate([p[2] for p in plan])
-        lv_d = torch.from_numpy(lv_all).to(dev)
     bound = max(level.ntot, 1)
     nb = _native.c_i64(0)
     lib.pcf_tree_level_workspace(bound, _native.ctypes.byref(nb))
