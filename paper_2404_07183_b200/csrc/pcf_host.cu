@@ -18,9 +18,12 @@
 //
 // Device buffers come from a grow-only workspace kept between calls (like a caching
 // allocator); pcf_release_workspace() frees it.
+#include <dlfcn.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <algorithm>
+#include <chrono>
 #include <numeric>
 #include <vector>
 #include "pcf_internal.h"
@@ -35,12 +38,12 @@ int fail(cudaError_t e, const char* where) {
 
 // grow-only device workspace, one slot per buffer role
 enum Slot { W_T, W_V, W_OFF, W_PERM, W_SOFF, W_GOFF, W_RECS, W_RECSG, W_TILE, W_ITEMS, W_CNT,
-            W_ERR, W_OUT, W_NSLOT };
+            W_ERR, W_OUT, W_TAG, W_DONE, W_NSLOT };
 struct Workspace {
   int device = -1;
   void* p[W_NSLOT] = {};
   size_t sz[W_NSLOT] = {};
-  cudaStream_t s0 = nullptr, s1 = nullptr;
+  cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;
   void release() {
     for (int k = 0; k < W_NSLOT; ++k) {
       if (p[k]) cudaFree(p[k]);
@@ -49,7 +52,8 @@ struct Workspace {
     }
     if (s0) cudaStreamDestroy(s0);
     if (s1) cudaStreamDestroy(s1);
-    s0 = s1 = nullptr;
+    if (s2) cudaStreamDestroy(s2);
+    s0 = s1 = s2 = nullptr;
     device = -1;
   }
   cudaError_t get(Slot k, size_t bytes, void** out) {
@@ -73,7 +77,8 @@ Workspace g_ws;
 cudaError_t copy_rows(const std::vector<int32_t>& perm, int64_t s0, int64_t s1, const char* dsrc,
                       char* hdst, int64_t M, int64_t ld, size_t es, cudaStream_t st) {
   const size_t n = (size_t)(s1 - s0);
-  if (n == 0) return cudaSuccess;
+  static const bool no_d2h = getenv("PCF_HOST_NO_D2H") != nullptr;  // timing experiments
+  if (n == 0 || no_d2h) return cudaSuccess;
   std::vector<void*> dst(n), src(n);
   std::vector<size_t> sizes(n, (size_t)M * es);
   for (size_t k = 0; k < n; ++k) {
@@ -95,6 +100,23 @@ cudaError_t copy_rows(const std::vector<int32_t>& perm, int64_t s0, int64_t s1, 
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// cuStreamWaitValue32 from the driver (opened at run time; null if unavailable): lets the
+// copy stream wait on the fill kernel's per-chunk completion counters, so the whole
+// matrix runs as ONE persistent launch (no per-chunk launch tails)
+typedef int (*WaitValue32)(void* stream, unsigned long long addr, unsigned int value,
+                           unsigned int flags);
+WaitValue32 stream_wait_fn() {
+  static WaitValue32 fn = [] {
+    if (getenv("PCF_NO_STREAM_WAIT")) return (WaitValue32) nullptr;
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return (WaitValue32) nullptr;
+    void* f = dlsym(h, "cuStreamWaitValue32_v2");
+    if (!f) f = dlsym(h, "cuStreamWaitValue32");
+    return (WaitValue32)f;
+  }();
+  return fn;
 }
 
 }  // namespace
@@ -127,14 +149,21 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   }
   if (!g_ws.s0) {
     if ((e = cudaStreamCreateWithFlags(&g_ws.s0, cudaStreamNonBlocking)) ||
-        (e = cudaStreamCreateWithFlags(&g_ws.s1, cudaStreamNonBlocking)))
+        (e = cudaStreamCreateWithFlags(&g_ws.s1, cudaStreamNonBlocking)) ||
+        (e = cudaStreamCreateWithFlags(&g_ws.s2, cudaStreamNonBlocking)))
       return fail(e, "pcf_matrix_host streams");
   }
   // compute on the caller's stream (events around the call then bracket all of its
   // device work), copies on a second stream joined back into it before returning
-  cudaStream_t s0 = stream ? (cudaStream_t)stream : g_ws.s0, s1 = g_ws.s1;
+  cudaStream_t s0 = stream ? (cudaStream_t)stream : g_ws.s0, s1 = g_ws.s1, s2 = g_ws.s2;
 
   // ---- host: size sort (descending, stable), sorted offsets, group offsets, plan
+  const bool timing = getenv("PCF_HOST_TIMING") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto ms_since = [&](std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+        .count();
+  };
   const int64_t N = off[M] - off[0];
   std::vector<int64_t> sizes(M);
   for (int64_t i = 0; i < M; ++i) {
@@ -218,6 +247,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
                      });
   }
 
+  const double host_ms = ms_since(t_start);
   // ---- device buffers
   const size_t es = is_f32 ? 4 : 8;
   void *d_t, *d_v, *d_off, *d_perm, *d_soff, *d_goff, *d_recs, *d_recsg, *d_tile, *d_items,
@@ -301,7 +331,55 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   std::vector<cudaEvent_t> evs(chunks.size(), nullptr);
   int64_t row_done = 0;
   int status = PCF_OK;
-  for (size_t k = 0; k < chunks.size() && status == PCF_OK; ++k) {
+  bool one_mode = n_items > 0;
+  for (int64_t i = 1; i < n_items && one_mode; ++i)
+    one_mode = items[i].smem_mode == items[0].smem_mode;
+  const WaitValue32 wait = stream_wait_fn();
+  bool single = false;
+  if (one_mode && wait) {
+    // ONE persistent launch over the row-block-ordered queue; item i bumps
+    // done[chunk(i)]; the copy stream waits for each chunk's count, then drains its rows
+    std::vector<int32_t> tag(n_items);
+    for (size_t k = 0; k < chunks.size(); ++k)
+      for (int64_t i = chunks[k].i0; i < chunks[k].i1; ++i) tag[i] = (int32_t)k;
+    void *d_tag, *d_done;
+    cudaEvent_t zeroed = nullptr;
+    if ((e = g_ws.get(W_TAG, n_items * 4, &d_tag)) ||
+        (e = g_ws.get(W_DONE, chunks.size() * 4, &d_done)) ||
+        (e = cudaMemcpyAsync(d_tag, tag.data(), n_items * 4, cudaMemcpyHostToDevice, s0)) ||
+        (e = cudaMemsetAsync(d_done, 0, chunks.size() * 4, s0)) ||
+        (e = cudaEventCreateWithFlags(&zeroed, cudaEventDisableTiming)) ||
+        (e = cudaEventRecord(zeroed, s0)) || (e = cudaStreamWaitEvent(s1, zeroed, 0)) ||
+        (e = cudaStreamWaitEvent(s2, zeroed, 0)))
+      return fail(e, "pcf_matrix_host single-launch setup");
+    evs[0] = zeroed;  // destroyed with the others
+    A.items = (const PcfWorkItem*)d_items;
+    A.n_items = (int)n_items;
+    A.smem_mode = items[0].smem_mode;
+    A.item_tag = (const int32_t*)d_tag;
+    A.tag_done = (int32_t*)d_done;
+    if ((e = cudaMemsetAsync(d_cnt, 0, 4, s0)) || (e = launch_fill_tiles(A, s0)))
+      return fail(e, "pcf_matrix_host fill");
+    single = true;
+    for (size_t k = 0; k < chunks.size() && status == PCF_OK; ++k) {
+      // chunks alternate between two copy streams (more DMA in flight over PCIe)
+      cudaStream_t sc = (k & 1) ? s2 : s1;
+      const unsigned n_k = (unsigned)(chunks[k].i1 - chunks[k].i0);
+      int r = wait((void*)sc, (unsigned long long)((int32_t*)d_done + k), n_k, 0 /*GEQ*/);
+      if (r) {
+        set_error("pcf_matrix_host: cuStreamWaitValue32 failed (%d)", r);
+        status = PCF_ERR_CUDA;
+        break;
+      }
+      if ((e = copy_rows(perm, row_done, chunks[k].row_end, (const char*)d_out, (char*)out, M,
+                         ld, es, sc))) {
+        status = fail(e, "pcf_matrix_host drain");
+        break;
+      }
+      row_done = chunks[k].row_end;
+    }
+  }
+  for (size_t k = 0; !single && k < chunks.size() && status == PCF_OK; ++k) {
     const Chunk& ch = chunks[k];
     for (int64_t i = ch.i0; i < ch.i1;) {
       int64_t j = i;
@@ -329,6 +407,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   if (status == PCF_OK) {
     if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming)) ||
         (e = cudaEventRecord(join, s1)) || (e = cudaStreamWaitEvent(s0, join, 0)) ||
+        (e = cudaEventRecord(join, s2)) || (e = cudaStreamWaitEvent(s0, join, 0)) ||
         (e = cudaMemcpyAsync(&key, d_err, 8, cudaMemcpyDeviceToHost, s0)) ||
         (e = cudaStreamSynchronize(s0)))
       status = fail(e, "pcf_matrix_host sync");
@@ -336,9 +415,13 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   } else {
     cudaStreamSynchronize(s0);
     cudaStreamSynchronize(s1);
+    cudaStreamSynchronize(s2);
   }
   for (auto ev : evs)
     if (ev) cudaEventDestroy(ev);
+  if (timing)
+    fprintf(stderr, "pcf_matrix_host: host prep %.1f ms, total %.1f ms, %zu chunks, %lld items\n",
+            host_ms, ms_since(t_start), chunks.size(), (long long)n_items);
   if (status) return status;
   if (key != ~0ull) {
     if (err_i) *err_i = (int64_t)(key / (unsigned long long)M);

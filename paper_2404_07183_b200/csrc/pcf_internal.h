@@ -31,6 +31,10 @@ struct FillArgs {
   int smem_bytes;
   int rec_bytes;  // 16: float64 records, 8: float32 records (recs/recs8 point to Rec32)
   int num_sms;
+  // optional per-item completion counters (pcf_matrix_host): item i adds 1 to
+  // tag_done[item_tag[i]] after its stores; null = no signalling
+  const int32_t* item_tag = nullptr;
+  int32_t* tag_done = nullptr;
 };
 
 struct RowsArgs {

@@ -133,6 +133,15 @@ __device__ __forceinline__ void finish_entry(double acc, double hl, double p, in
   out[oj * ld + oi] = o;
 }
 
+// Completion signal of one work item (pcf_matrix_host's single-launch drain): called by
+// thread 0 after a barrier that follows the item's last store; the copy stream waits for
+// each chunk's counter (cuStreamWaitValue32) before copying its finished rows.
+__device__ __forceinline__ void signal_item(const int32_t* __restrict__ tag,
+                                            int32_t* __restrict__ done, int it) {
+  __threadfence_system();
+  atomicAdd(&done[tag[it]], 1);
+}
+
 // --------------------------------------------------------------------------------------
 // K1: persistent tile kernel (512 threads, one CTA per SM).
 //
@@ -155,7 +164,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                       const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
                       int n_items, int* __restrict__ counter, double p, double a, double b,
                       int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
-                      unsigned long long* __restrict__ err) {
+                      unsigned long long* __restrict__ err,
+                      const int32_t* __restrict__ item_tag, int32_t* __restrict__ tag_done) {
   // GW: rows per interleaved group = lanes per shared-memory phase for sizeof(RT)-byte
   // loads (8 x 16 B or 16 x 8 B = 128 B); CA: records per 16 B (bulk-copy granularity)
   constexpr int LOGGW = GW == 16 ? 4 : 3;
@@ -275,6 +285,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       }
     }
     __syncthreads();  // all finishers done before the next item reuses shared memory
+    if (tag_done && tid == 0) signal_item(item_tag, tag_done, it);
   }
 }
 
@@ -287,7 +298,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                         const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
                         int n_items, int* __restrict__ counter, double p, double a, double b,
                         int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
-                        unsigned long long* __restrict__ err) {
+                        unsigned long long* __restrict__ err,
+                      const int32_t* __restrict__ item_tag, int32_t* __restrict__ tag_done) {
   __shared__ int s_item;
   const int tid = threadIdx.x;
   for (;;) {
@@ -324,6 +336,10 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                                     (int64_t)perm[qs], out, ld, M, err);
       }
     }
+    if (tag_done) {
+      __syncthreads();
+      if (tid == 0) signal_item(item_tag, tag_done, it);
+    }
   }
 }
 
@@ -345,7 +361,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                   const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
                   int n_items, int* __restrict__ counter, double p, double a, double b,
                   int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
-                  unsigned long long* __restrict__ err) {
+                  unsigned long long* __restrict__ err,
+                      const int32_t* __restrict__ item_tag, int32_t* __restrict__ tag_done) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RT* rowS = reinterpret_cast<RT*>(smem_raw);
   __shared__ int s_item;
@@ -385,6 +402,10 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         finish_entry<BOUNDED, OutT>(acc, hl, p, apply_root, (int64_t)perm[ps],
                                     (int64_t)perm[qs], out, ld, M, err);
       }
+    }
+    if (tag_done) {
+      __syncthreads();
+      if (tid == 0) signal_item(item_tag, tag_done, it);
     }
   }
 }
@@ -633,14 +654,14 @@ static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
           (const Rec32*)A.recs, (const Rec32*)A.recs8, A.soff, A.goff8, A.perm, A.items,
-          A.n_items, A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+          A.n_items, A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
     } else {
       auto kern = k_fill_tiles_smem<HK, BOUNDED, OutT, Rec, 8>;
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
       if (e != cudaSuccess) return e;
       kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
           (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
-          A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+          A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
     }
   } else if (A.smem_mode == 2) {
     const size_t sm = (size_t)A.smem_bytes;
@@ -651,23 +672,23 @@ static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       k_fill_rowres<HK, BOUNDED, OutT, Rec32><<<grid, kTileThreads, sm, st>>>(
           (const Rec32*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
-          A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+          A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
     } else {
       e = cudaFuncSetAttribute(k_fill_rowres<HK, BOUNDED, OutT, Rec>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
       k_fill_rowres<HK, BOUNDED, OutT, Rec><<<grid, kTileThreads, sm, st>>>(
           (const Rec*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
-          A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+          A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
     }
   } else if (A.rec_bytes == 8) {
     k_fill_tiles_global<HK, BOUNDED, OutT, Rec32><<<grid * 2, kTileThreads, 0, st>>>(
         (const Rec32*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
-        A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+        A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
   } else {
     k_fill_tiles_global<HK, BOUNDED, OutT, Rec><<<grid * 2, kTileThreads, 0, st>>>(
         (const Rec*)A.recs, A.soff, A.perm, A.items, A.n_items, A.counter, A.p, A.a, A.b,
-        A.apply_root, (OutT*)A.out, A.ld, A.M, A.err);
+        A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
   }
   return cudaGetLastError();
 }
