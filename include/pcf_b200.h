@@ -234,14 +234,26 @@ int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
                    int64_t ntot, void* t_out_dev, void* v_out_dev, double* v2_out_dev,
                    int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, int32_t* status_dev,
                    void* stream);
-/* mean finalisation: v * T(scale[seg]) (core.scale) + keep-where-changed flags. */
-int pcf_scale_flag(int is_f32, const void* v_dev, const int64_t* off_dev, int64_t nseg,
-                   const double* scale_dev, int64_t ntot, void* sv_dev, int32_t* flag_dev,
-                   int32_t* status_dev, void* stream);
-/* variance / std finalisation from M2: T(M2 * scale[seg]) [then T(sqrt(.))] + flags. */
-int pcf_std_flag(int is_f32, int take_sqrt, const double* m2_dev, const int64_t* off_dev,
-                 int64_t nseg, const double* scale_dev, int64_t ntot, void* sv_dev,
-                 int32_t* flag_dev, int32_t* status_dev, void* stream);
+/* Non-compacting level for (nearly) distinct breakpoint times: the same merge, every
+ * candidate kept at its own input position (node offsets unchanged).  A time present in
+ * both children yields a zero-width piece followed by the exact point; the finalisation
+ * drops zero-width pieces when given the times (t_dev below).  Same workspace. */
+int pcf_tree_merge_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
+                         const double* v2_dev, const int64_t* off_dev, const int64_t* src_dev,
+                         const int32_t* cnt_dev, const int64_t* leaves_dev, int64_t nout,
+                         int64_t ntot, void* t_out_dev, void* v_out_dev, double* v2_out_dev,
+                         int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, void* stream);
+/* mean finalisation: v * T(scale[seg]) (core.scale) + keep-where-changed flags.
+ * t_dev (optional): the node times; zero-width pieces (next point of the node at the same
+ * time) get flag 0 and survivors compare with the previous survivor. */
+int pcf_scale_flag(int is_f32, const void* v_dev, const void* t_dev, const int64_t* off_dev,
+                   int64_t nseg, const double* scale_dev, int64_t ntot, void* sv_dev,
+                   int32_t* flag_dev, int32_t* status_dev, void* stream);
+/* variance / std finalisation from M2: T(M2 * scale[seg]) [then T(sqrt(.))] + flags;
+ * t_dev as for pcf_scale_flag. */
+int pcf_std_flag(int is_f32, int take_sqrt, const double* m2_dev, const void* t_dev,
+                 const int64_t* off_dev, int64_t nseg, const double* scale_dev, int64_t ntot,
+                 void* sv_dev, int32_t* flag_dev, int32_t* status_dev, void* stream);
 
 #ifdef __cplusplus
 }

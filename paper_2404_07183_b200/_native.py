@@ -99,8 +99,12 @@ SIGNATURES = {
     "pcf_tree_level": (
         c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
                 c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
-    "pcf_scale_flag": (c_int, [c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
-    "pcf_std_flag": (c_int, [c_int, c_int, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
+    "pcf_tree_merge_level": (
+        c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+                c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pcf_scale_flag": (c_int, [c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
+                               c_vp]),
+    "pcf_std_flag": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp,
                              c_vp]),
 }
 

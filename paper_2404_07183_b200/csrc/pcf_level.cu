@@ -509,6 +509,276 @@ __global__ void k_fix_offsets(const int64_t* __restrict__ off, const int64_t* __
     off_out[k] += tile_excl[off[src[k]] / LT];
 }
 
+// Non-compacting level (K5m): the same merge as k_level_tiled, but every candidate is
+// kept at its own input position -- no keep flags, no scan, no look-back, node offsets
+// unchanged.  Used above the first level when breakpoints are (nearly) distinct, where
+// compaction would drop almost nothing.  A breakpoint time present in both children
+// yields two consecutive points with the same time: the first is a zero-width piece
+// (its value combines one child's jump with the other child's previous value, which the
+// reference never forms), the second carries the exact reference value.  Survivors only
+// ever combine survivors, so every last-of-its-time point equals the reference tree value
+// bit for bit; the finalisation (k_scale_flag / k_std_flag with times) drops zero-width
+// pieces and then minimises, which is the reference's result (intermediate emission
+// never changes values, only which redundant points exist).
+template <typename T, int K>
+__global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
+    k_merge_level(const T* __restrict__ t, const void* __restrict__ v_,
+                  const double* __restrict__ v2, const int64_t* __restrict__ off,
+                  const int64_t* __restrict__ src, const int32_t* __restrict__ cnt,
+                  const int64_t* __restrict__ leaves, int64_t nout,
+                  const int64_t* __restrict__ tile_node, const int64_t* __restrict__ tile_i,
+                  T* __restrict__ t_out, void* __restrict__ v_out_, double* __restrict__ v2_out) {
+  using VT = typename std::conditional<K == K_MOM, double, T>::type;
+  const VT* __restrict__ v = reinterpret_cast<const VT*>(v_);
+  VT* __restrict__ v_out = reinterpret_cast<VT*>(v_out_);
+  constexpr bool MOM = (K == K_MOM);
+  constexpr int WCAP = wcap<T>();
+  constexpr int U = 16 / (int)sizeof(T);
+
+  __shared__ Seg seg[MAXSEG];
+  __shared__ int seg_pos[MAXSEG + 1];
+  extern __shared__ __align__(16) unsigned char dyn[];
+  VT* s_v = reinterpret_cast<VT*>(dyn);
+  double* s_v2 = reinterpret_cast<double*>(dyn + WCAP * sizeof(VT));
+  T* s_t = reinterpret_cast<T*>(dyn + WCAP * sizeof(VT) + (MOM ? WCAP * sizeof(double) : 0));
+  __shared__ uint64_t s_bar;
+  __shared__ int64_t s_next_node, s_round_end;
+  typedef cub::BlockScan<int, LTH> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
+  uint32_t bar_phase = 0;
+  __syncthreads();
+  const int64_t tile = blockIdx.x;
+  const int64_t ntot = off[src[nout - 1] + cnt[nout - 1]];
+  const int64_t e0 = tile * (int64_t)LT;
+  if (e0 >= ntot) return;
+  const int64_t e1 = min(e0 + (int64_t)LT, ntot);
+  int64_t kr = tile_node[tile];
+  int64_t rs = e0;
+  while (rs < e1) {
+    int valid = 0;
+    {
+      const int64_t kk = kr + tid;
+      if (tid < MAXSEG && kk < nout) {
+        const int64_t s = src[kk];
+        const int c = cnt[kk];
+        const int64_t b = off[s];
+        const int64_t la = off[s + 1] - b;
+        const int64_t lb = (c == 2) ? off[s + 2] - off[s + 1] : 0;
+        const int64_t ss = max(rs, b), se = min(e1, b + la + lb);
+        if (ss < se) {
+          valid = 1;
+          Seg g;
+          g.node = kk;
+          g.base = b;
+          g.na = la;
+          g.nb = lb;
+          g.m0 = ss - b;
+          g.m1 = se - b;
+          g.pass = (c == 1);
+          if (g.pass) {
+            g.i0 = g.m0; g.j0 = 0; g.i1 = g.m1; g.j1 = 0;
+          } else {
+            g.i0 = g.m0 == 0 ? 0 : tile_i[tile];
+            g.j0 = g.m0 - g.i0;
+            g.i1 = g.m1 == la + lb ? la : tile_i[tile + 1];
+            g.j1 = g.m1 - g.i1;
+          }
+          g.ia_lo = g.i0 > 0 ? g.i0 - 1 : 0;
+          g.jb_lo = g.j0 > 0 ? g.j0 - 1 : 0;
+          g.alen = (int)(min(g.i1 + 1, la) - g.ia_lo);
+          g.blen = lb > 0 ? (int)(min(g.j1 + 1, lb) - g.jb_lo) : 0;
+          g.ga = b + g.ia_lo;
+          g.gb = b + la + g.jb_lo;
+          if (MOM && !g.pass) {
+            const double nA = (double)leaves[s], nB = (double)leaves[s + 1];
+            const double n = nA + nB;
+            g.wB = nB / n;
+            g.wAB = nA * nB / n;
+          } else {
+            g.wB = g.wAB = 0.0;
+          }
+          seg[tid] = g;
+        }
+      }
+    }
+    const int nseg = __syncthreads_count(valid);
+    int la_p = 0, lb_p = 0;
+    if (tid < nseg) {
+      const Seg& g = seg[tid];
+      la_p = (int)(((g.ga + g.alen + U - 1) & ~(int64_t)(U - 1)) - (g.ga & ~(int64_t)(U - 1)));
+      lb_p = g.blen > 0 ? (int)(((g.gb + g.blen + U - 1) & ~(int64_t)(U - 1)) -
+                                (g.gb & ~(int64_t)(U - 1)))
+                        : 0;
+    }
+    int woff, wtot;
+    Scan(scan_tmp).ExclusiveSum(la_p + lb_p, woff, wtot);
+    if (tid < nseg) {
+      seg[tid].aoff = woff + (int)(seg[tid].ga & (U - 1));
+      seg[tid].boff = woff + la_p + (int)(seg[tid].gb & (U - 1));
+      seg_pos[tid] = (int)(seg[tid].base + seg[tid].m0 - rs);
+    }
+    if (tid == 0) {
+      const Seg& last = seg[nseg - 1];
+      s_round_end = last.base + last.m1;
+      s_next_node = kr + nseg;
+      seg_pos[nseg] = (int)(s_round_end - rs);
+    }
+    if (tid < nseg) {
+      const Seg g = seg[tid];
+      fence_proxy_async();
+      uint32_t bytes = 0;
+      int64_t lo_[2], hi_[2];
+      int dst_[2];
+      lo_[0] = g.ga & ~(int64_t)(U - 1);
+      hi_[0] = (g.ga + g.alen) & ~(int64_t)(U - 1);
+      dst_[0] = woff;
+      lo_[1] = g.gb & ~(int64_t)(U - 1);
+      hi_[1] = g.blen > 0 ? ((g.gb + g.blen) & ~(int64_t)(U - 1)) : lo_[1];
+      dst_[1] = woff + la_p;
+      for (int w = 0; w < 2; ++w)
+        if (hi_[w] > lo_[w])
+          bytes += (uint32_t)((hi_[w] - lo_[w]) * (sizeof(T) + sizeof(VT) + (MOM ? 8 : 0)));
+      if (bytes) mbar_expect_tx(&s_bar, bytes);
+      for (int w = 0; w < 2; ++w) {
+        if (hi_[w] > lo_[w]) {
+          const uint32_t n = (uint32_t)(hi_[w] - lo_[w]);
+          bulk_g2s(s_t + dst_[w], t + lo_[w], n * (uint32_t)sizeof(T), &s_bar);
+          bulk_g2s(s_v + dst_[w], v + lo_[w], n * (uint32_t)sizeof(VT), &s_bar);
+          if (MOM) bulk_g2s(s_v2 + dst_[w], v2 + lo_[w], n * 8u, &s_bar);
+        }
+        const int64_t e = w == 0 ? g.ga + g.alen : (g.blen > 0 ? g.gb + g.blen : 0);
+        for (int64_t x = max(hi_[w], lo_[w]); x < e; ++x) {
+          const int d = dst_[w] + (int)(x - lo_[w]);
+          s_t[d] = t[x];
+          s_v[d] = v[x];
+          if (MOM) s_v2[d] = v2[x];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) mbar_arrive(&s_bar);
+    const int64_t re = s_round_end;
+    mbar_wait(&s_bar, bar_phase);
+    bar_phase ^= 1u;
+    __syncthreads();
+    // ---- walk: every candidate is written at its own position rs + p
+    const int p0 = tid * LPT;
+    const int rlen = (int)(re - rs);
+    if (p0 < rlen) {
+      int sg;
+      {
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (seg_pos[mid] <= p0) lo = mid;
+          else hi = mid - 1;
+        }
+        sg = lo;
+      }
+      Seg g = seg[sg];
+      int i = 0, j = 0;
+      const T* pa_t;
+      const T* pb_t;
+      const VT* pa_v;
+      const VT* pb_v;
+      const double* pa_2;
+      const double* pb_2;
+      auto bind = [&]() {
+        pa_t = s_t + g.aoff - (int)g.ia_lo;
+        pb_t = s_t + g.boff - (int)g.jb_lo;
+        pa_v = s_v + g.aoff - (int)g.ia_lo;
+        pb_v = s_v + g.boff - (int)g.jb_lo;
+        pa_2 = s_v2 + g.aoff - (int)g.ia_lo;
+        pb_2 = s_v2 + g.boff - (int)g.jb_lo;
+      };
+      bind();
+      const T TINF = (T)INFINITY;
+      T tai = TINF, tbj = TINF;
+      auto start = [&](int mm) {
+        if (g.pass) {
+          i = mm;
+          j = 0;
+          return;
+        }
+        int lo = max((int)g.i0, mm - (int)g.j1), hi = min((int)g.i1, mm - (int)g.j0);
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (pa_t[mid] <= pb_t[mm - mid - 1]) lo = mid + 1;
+          else hi = mid;
+        }
+        i = lo;
+        j = mm - lo;
+        tai = i < (int)g.na ? pa_t[i] : TINF;
+        tbj = j < (int)g.nb ? pb_t[j] : TINF;
+      };
+      start((int)g.m0 + (p0 - seg_pos[sg]));
+      int64_t pos = rs + p0;
+#pragma unroll
+      for (int q = 0; q < LPT; ++q) {
+        const int p = p0 + q;
+        if (p < rlen) {
+          if (sg + 1 < nseg && p >= seg_pos[sg + 1]) {
+            ++sg;
+            g = seg[sg];
+            bind();
+            start((int)g.m0);
+          }
+          T tt;
+          VT val;
+          double val2 = 0.0;
+          if (g.pass) {
+            tt = pa_t[i];
+            val = pa_v[i];
+            if (MOM) val2 = pa_2[i];
+            ++i;
+          } else {
+            const bool takeA = tai <= tbj;  // A first on ties (stable merge)
+            tt = takeA ? tai : tbj;
+            const int ia = takeA ? i : i - 1;
+            int ib = takeA ? j - 1 : j;
+            ib = ib < 0 ? 0 : ib;  // a t = 0 zero-width piece before B's first point
+            if (MOM) {
+              const double d = (double)pb_v[ib] - (double)pa_v[ia];
+              val = (VT)((double)pa_v[ia] + d * g.wB);
+              val2 = (pa_2[ia] + pb_2[ib]) + d * d * g.wAB;
+            } else {
+              val = to_t<VT>(vop<K>((double)pa_v[ia], (double)pb_v[ib]));
+            }
+            i += takeA ? 1 : 0;
+            j += takeA ? 0 : 1;
+            const bool inA = takeA ? (i < (int)g.na) : (j < (int)g.nb);
+            const T nxt = inA ? (takeA ? pa_t[i] : pb_t[j]) : TINF;
+            tai = takeA ? nxt : tai;
+            tbj = takeA ? tbj : nxt;
+          }
+          t_out[pos] = tt;
+          v_out[pos] = val;
+          if (MOM) v2_out[pos] = val2;
+          ++pos;
+        }
+      }
+    }
+    rs = re;
+    kr = s_next_node;
+    __syncthreads();
+  }
+}
+
+// Output node offsets of a non-compacting level: node k starts where its first child did.
+__global__ void k_merge_offsets(const int64_t* __restrict__ off, const int64_t* __restrict__ src,
+                                const int32_t* __restrict__ cnt, int64_t nout,
+                                int64_t* __restrict__ off_out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= nout;
+       k += (int64_t)gridDim.x * blockDim.x)
+    off_out[k] = k < nout ? off[src[k]] : off[src[nout - 1] + cnt[nout - 1]];
+}
+
 // Merge-path partition: for every tile start (and the end of the last tile) the output
 // node containing it (largest k with off[src[k]] <= e) and the co-rank (A elements among
 // the node's first m candidates).
@@ -643,5 +913,72 @@ int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
   }
   return PCF_OK;
 }
+
+int pcf_tree_merge_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
+                         const double* v2_dev, const int64_t* off_dev, const int64_t* src_dev,
+                         const int32_t* cnt_dev, const int64_t* leaves_dev, int64_t nout,
+                         int64_t ntot, void* t_out_dev, void* v_out_dev, double* v2_out_dev,
+                         int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nout <= 0) return PCF_OK;
+  if (kind < 0 || kind > 4 || !t_dev || !v_dev || !off_dev || !src_dev || !cnt_dev ||
+      !t_out_dev || !v_out_dev || !off_out_dev || !ws_dev ||
+      (kind == K_MOM && (!v2_dev || !v2_out_dev || !leaves_dev))) {
+    set_error("pcf_tree_merge_level: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  const int og = (int)((nout + 1 + 255) / 256 < 4096 ? (nout + 1 + 255) / 256 : 4096);
+  k_merge_offsets<<<og, 256, 0, s>>>(off_dev, src_dev, cnt_dev, nout, off_out_dev);
+  if (ntot <= 0) return PCF_OK;
+  const int64_t ntiles = (ntot + LT - 1) / LT;
+  int64_t need = 0;
+  pcf_tree_level_workspace(ntot, &need);
+  if (ws_bytes < need) {
+    set_error("pcf_tree_merge_level: workspace %lld < %lld bytes", (long long)ws_bytes,
+              (long long)need);
+    return PCF_ERR_ARG;
+  }
+  int64_t* tile_node = (int64_t*)ws_dev;
+  int64_t* tile_i = tile_node + (ntiles + 1);
+  const int pg = (int)((ntiles + 1 + 255) / 256);
+  const unsigned grid = (unsigned)ntiles;
+#define PCF_ML(T, K)                                                                          \
+  do {                                                                                        \
+    typedef typename std::conditional<K == K_MOM, double, T>::type VT_;                      \
+    const int dsm = wcap<T>() * (int)(sizeof(VT_) + sizeof(T) + (K == K_MOM ? sizeof(double) : 0)); \
+    k_tile_part<T><<<pg, 256, 0, s>>>((const T*)t_dev, off_dev, src_dev, cnt_dev, nout, ntot, \
+                                      ntiles, tile_node, tile_i);                             \
+    cudaFuncSetAttribute(k_merge_level<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                         dsm);                                                                \
+    k_merge_level<T, K><<<grid, LTH, dsm, s>>>((const T*)t_dev, v_dev, v2_dev, off_dev,       \
+                                               src_dev, cnt_dev, leaves_dev, nout, tile_node, \
+                                               tile_i, (T*)t_out_dev, v_out_dev, v2_out_dev); \
+  } while (0)
+  if (is_f32) {
+    switch (kind) {
+      case K_ADD: PCF_ML(float, K_ADD); break;
+      case K_MAX: PCF_ML(float, K_MAX); break;
+      case K_MIN: PCF_ML(float, K_MIN); break;
+      case K_MUL: PCF_ML(float, K_MUL); break;
+      default: PCF_ML(float, K_MOM); break;
+    }
+  } else {
+    switch (kind) {
+      case K_ADD: PCF_ML(double, K_ADD); break;
+      case K_MAX: PCF_ML(double, K_MAX); break;
+      case K_MIN: PCF_ML(double, K_MIN); break;
+      case K_MUL: PCF_ML(double, K_MUL); break;
+      default: PCF_ML(double, K_MOM); break;
+    }
+  }
+#undef PCF_ML
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("pcf_tree_merge_level: %s", cudaGetErrorString(e));
+    return PCF_ERR_CUDA;
+  }
+  return PCF_OK;
+}
+
 
 }  // extern "C"

@@ -58,9 +58,37 @@ __global__ void k_out_offsets(const int64_t* __restrict__ off_in, const int64_t*
 // mean: v * T(scale) in T arithmetic (core.scale, core.py:172), then keep where the value
 // changes (minimize_discretization, core.py:189-203).  Per-segment scale factors allow a
 // batch of independent means (mean_along).
+// Zero-width pieces (non-compacting levels, k_merge_level): point e is dropped when the
+// next point of its node has the same time; a surviving point is compared with the last
+// survivor before it, i.e. the point just before its run of equal times.
 template <typename T>
-__global__ void k_scale_flag(const T* __restrict__ v, const int64_t* __restrict__ off,
-                             int64_t nseg, const double* __restrict__ scale, int64_t ntot,
+__device__ __forceinline__ bool zero_width(const T* __restrict__ t, int64_t e, int64_t end) {
+  return t && e + 1 < end && t[e + 1] == t[e];
+}
+
+template <typename T>
+__device__ __forceinline__ int64_t prev_survivor(const T* __restrict__ t, int64_t e,
+                                                 int64_t begin) {
+  if (!t || e == begin || t[e - 1] != t[e]) return e - 1;
+  // node times are non-decreasing: binary search for the start of e's run of equal times
+  // (the t = 0 run of a non-compacting tree holds one point per merged level)
+  int64_t lo = begin, hi = e;
+  const T te = t[e];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (t[mid] < te) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo - 1;
+}
+
+// mean: v * T(scale) in T arithmetic (core.scale, core.py:172), then keep where the value
+// changes (minimize_discretization, core.py:189-203).  Per-segment scale factors allow a
+// batch of independent means (mean_along).  t (optional): drop zero-width pieces first.
+template <typename T>
+__global__ void k_scale_flag(const T* __restrict__ v, const T* __restrict__ t,
+                             const int64_t* __restrict__ off, int64_t nseg,
+                             const double* __restrict__ scale, int64_t ntot,
                              T* __restrict__ sv, int32_t* __restrict__ flag,
                              int32_t* __restrict__ status) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ntot;
@@ -74,21 +102,22 @@ __global__ void k_scale_flag(const T* __restrict__ v, const int64_t* __restrict_
     const T a = to_t<T>(scale[lo]);
     const T x = v[e] * a;
     sv[e] = x;
-    if (!isfinite((double)x)) atomicOr(status, 1);
-    if (e == off[lo]) {
-      flag[e] = 1;
-    } else {
-      const T y = v[e - 1] * a;
-      flag[e] = (x != y);
+    if (zero_width(t, e, off[lo + 1])) {
+      flag[e] = 0;
+      continue;
     }
+    if (!isfinite((double)x)) atomicOr(status, 1);
+    const int64_t p = prev_survivor(t, e, off[lo]);
+    flag[e] = (p < off[lo]) ? 1 : (x != v[p] * a);
   }
 }
 
 // std: s = T(sqrt(double(T(M2 * scale)))) (variance scale in float64, then
 // core.apply_unary(math.sqrt)), keep where s changes.
 template <typename T, bool SQRT>
-__global__ void k_std_flag(const double* __restrict__ m2, const int64_t* __restrict__ off,
-                           int64_t nseg, const double* __restrict__ scale, int64_t ntot,
+__global__ void k_std_flag(const double* __restrict__ m2, const T* __restrict__ t,
+                           const int64_t* __restrict__ off, int64_t nseg,
+                           const double* __restrict__ scale, int64_t ntot,
                            T* __restrict__ sv, int32_t* __restrict__ flag,
                            int32_t* __restrict__ status) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ntot;
@@ -106,8 +135,13 @@ __global__ void k_std_flag(const double* __restrict__ m2, const int64_t* __restr
     };
     const T x = sd(e);
     sv[e] = x;
+    if (zero_width(t, e, off[lo + 1])) {
+      flag[e] = 0;
+      continue;
+    }
     if (!isfinite((double)x)) atomicOr(status, 1);
-    flag[e] = (e == off[lo]) ? 1 : (x != sd(e - 1));
+    const int64_t p = prev_survivor(t, e, off[lo]);
+    flag[e] = (p < off[lo]) ? 1 : (x != sd(p));
   }
 }
 
@@ -180,18 +214,19 @@ int pcf_compact(int is_f32, const void* st_dev, const void* sv_dev, const void* 
   return PCF_OK;
 }
 
-int pcf_scale_flag(int is_f32, const void* v_dev, const int64_t* off_dev, int64_t nseg,
-                   const double* scale_dev, int64_t ntot, void* sv_dev, int32_t* flag_dev,
-                   int32_t* status_dev, void* stream) {
+int pcf_scale_flag(int is_f32, const void* v_dev, const void* t_dev, const int64_t* off_dev,
+                   int64_t nseg, const double* scale_dev, int64_t ntot, void* sv_dev,
+                   int32_t* flag_dev, int32_t* status_dev, void* stream) {
   if (ntot <= 0) return PCF_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int g = grid_for(ntot, 256);
   if (is_f32)
-    k_scale_flag<float><<<g, 256, 0, s>>>((const float*)v_dev, off_dev, nseg, scale_dev, ntot,
-                                          (float*)sv_dev, flag_dev, status_dev);
+    k_scale_flag<float><<<g, 256, 0, s>>>((const float*)v_dev, (const float*)t_dev, off_dev, nseg,
+                                          scale_dev, ntot, (float*)sv_dev, flag_dev, status_dev);
   else
-    k_scale_flag<double><<<g, 256, 0, s>>>((const double*)v_dev, off_dev, nseg, scale_dev, ntot,
-                                           (double*)sv_dev, flag_dev, status_dev);
+    k_scale_flag<double><<<g, 256, 0, s>>>((const double*)v_dev, (const double*)t_dev, off_dev,
+                                           nseg, scale_dev, ntot, (double*)sv_dev, flag_dev,
+                                           status_dev);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("pcf_scale_flag: %s", cudaGetErrorString(e));
@@ -200,15 +235,15 @@ int pcf_scale_flag(int is_f32, const void* v_dev, const int64_t* off_dev, int64_
   return PCF_OK;
 }
 
-int pcf_std_flag(int is_f32, int take_sqrt, const double* m2_dev, const int64_t* off_dev,
-                 int64_t nseg, const double* scale_dev, int64_t ntot, void* sv_dev,
-                 int32_t* flag_dev, int32_t* status_dev, void* stream) {
+int pcf_std_flag(int is_f32, int take_sqrt, const double* m2_dev, const void* t_dev,
+                 const int64_t* off_dev, int64_t nseg, const double* scale_dev, int64_t ntot,
+                 void* sv_dev, int32_t* flag_dev, int32_t* status_dev, void* stream) {
   if (ntot <= 0) return PCF_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int g = grid_for(ntot, 256);
 #define PCF_SF(T, SQ)                                                                      \
-  k_std_flag<T, SQ><<<g, 256, 0, s>>>(m2_dev, off_dev, nseg, scale_dev, ntot, (T*)sv_dev, \
-                                      flag_dev, status_dev)
+  k_std_flag<T, SQ><<<g, 256, 0, s>>>(m2_dev, (const T*)t_dev, off_dev, nseg, scale_dev, ntot, \
+                                      (T*)sv_dev, flag_dev, status_dev)
   if (is_f32) {
     if (take_sqrt) PCF_SF(float, true); else PCF_SF(float, false);
   } else {

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import math
 import operator
+import os
 
 import numpy as np
 
@@ -206,18 +207,30 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
     so = lo = 0
     cur_t, cur_v, cur_m2, cur_off = level.t, level.v, level.m2, level.off
     nout = level.nnodes
+    mode = os.environ.get("PCF_TREE_MODE", "auto")  # auto | compact | merge
+    merge = mode == "merge"
     for li, (src, cnt, _) in enumerate(plan):
         nout = src.shape[0]
         t_out, v_out, m2_out = bufs[li % 2]
         off_out = torch.empty(nout + 1, dtype=torch.int64, device=dev)
-        _native.check(lib.pcf_tree_level(
-            kind, int(level.is_f32), _native.ptr(cur_t), _native.ptr(cur_v),
-            _native.ptr(cur_m2) if moments else None, _native.ptr(cur_off),
-            _native.c_vp(src_d.data_ptr() + 8 * so), _native.c_vp(cnt_d.data_ptr() + 4 * so),
-            _native.c_vp(lv_d.data_ptr() + 8 * lo) if moments else None,
-            nout, bound, _native.ptr(t_out), _native.ptr(v_out),
-            _native.ptr(m2_out) if moments else None, _native.ptr(off_out), _native.ptr(ws),
-            ws.numel(), _native.ptr(status), st), "pcf_tree_level")
+        args = (int(level.is_f32), _native.ptr(cur_t), _native.ptr(cur_v),
+                _native.ptr(cur_m2) if moments else None, _native.ptr(cur_off),
+                _native.c_vp(src_d.data_ptr() + 8 * so), _native.c_vp(cnt_d.data_ptr() + 4 * so),
+                _native.c_vp(lv_d.data_ptr() + 8 * lo) if moments else None,
+                nout, bound, _native.ptr(t_out), _native.ptr(v_out),
+                _native.ptr(m2_out) if moments else None, _native.ptr(off_out), _native.ptr(ws),
+                ws.numel())
+        if merge and li > 0:
+            # non-compacting merge (zero-width pieces are dropped by _finalize)
+            _native.check(lib.pcf_tree_merge_level(kind, *args, st), "pcf_tree_merge_level")
+        else:
+            _native.check(lib.pcf_tree_level(kind, *args, _native.ptr(status), st),
+                          "pcf_tree_level")
+        if li == 0 and len(plan) > 1 and mode == "auto":
+            # nearly distinct breakpoints (compaction kept >= 90% of level 0): the upper
+            # levels would drop almost nothing, so they run without compaction
+            kept = int(off_out[-1].item())
+            merge = kept >= 0.9 * level.ntot
         so += nout
         if moments:
             lo += plan[li][2].shape[0]
@@ -243,12 +256,14 @@ def _finalize(level: DeviceLevel, scales, kind, take_sqrt=False):
     sc = torch.tensor(np.asarray(scales, dtype=np.float64), device=dev)
     if kind == "scale":
         _native.check(lib.pcf_scale_flag(int(level.is_f32), _native.ptr(level.v),
+                                         _native.ptr(level.t),
                                          _native.ptr(level.off), level.nnodes, _native.ptr(sc), n,
                                          _native.ptr(sv), _native.ptr(flag), _native.ptr(status),
                                          st), "pcf_scale_flag")
     else:
         _native.check(lib.pcf_std_flag(int(level.is_f32), int(take_sqrt), _native.ptr(level.m2),
-                                       _native.ptr(level.off), level.nnodes, _native.ptr(sc), n,
+                                       _native.ptr(level.t), _native.ptr(level.off),
+                                       level.nnodes, _native.ptr(sc), n,
                                        _native.ptr(sv), _native.ptr(flag), _native.ptr(status),
                                        st), "pcf_std_flag")
     _check_status(status, "scaling")
