@@ -48,7 +48,6 @@ __device__ __forceinline__ double pcf_pymod(double x, double y) {
   return r;
 }
 __device__ __forceinline__ double pcf_sq(double x) { return __dmul_rn(x, x); }
-__device__ __forceinline__ double pcf_truth(double x) { return x != 0.0 ? 1.0 : 0.0; }
 
 // max{i < n : key(i) <= a} + 1 style start cursor: number of records whose piece ends at
 // or before a (the reference's linear _start_index, sweep.py:59-64)

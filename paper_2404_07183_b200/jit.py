@@ -11,8 +11,8 @@ through NVRTC for sm_100a.  Modules are cached per generated source.
 
 Supported: lambdas and single-expression functions (optionally with local assignments
 before the ``return``) over float arguments, using arithmetic, comparisons, conditional
-expressions, ``abs``/``min``/``max``/``pow``/``float``/``round``-free builtins, ``math``
-functions and constants, the matching ``numpy`` ufuncs (``np.abs``, ``np.maximum``,
+expressions, the builtins ``abs``/``min``/``max``/``pow``/``float``, ``math`` functions
+and constants, the matching ``numpy`` ufuncs (``np.abs``, ``np.maximum``,
 ``np.exp``, ...), numeric constants and numeric closure/global variables (inlined
 exactly as hexadecimal literals), and calls to other such functions.  Anything else
 raises :class:`errors.UnsupportedIntegrand` -- there is no CPU fallback.

@@ -63,8 +63,7 @@ def test_combination_integrals_match_reference(gold, ctag, name):
         return
     ci = pb.CombinationIntegral(h=fns.get("h"), H=fns.get("H"), r=fns.get("r"), a=a, b=b,
                                 symmetric=sym)
-    job = pb.pairwise_job(fs, ci)
-    D = job.run().data if False else np.asarray(pb.pairwise(fs, ci))
+    D = np.asarray(pb.pairwise(fs, ci))
     ref = gold[key]
     assert D.dtype == ref.dtype and D.shape == ref.shape
     assert close(D, ref, exact), np.max(np.abs(D - ref))
