@@ -56,7 +56,8 @@ typedef struct pcf_work_item {
   int32_t nrows;     /* rows in the block (K1: 8 or 16 = one or two interleaved groups) */
   int32_t col0;      /* first size-sorted column of this item */
   int32_t col1;      /* one past the last column */
-  int32_t logC;      /* columns per streamed chunk = 1 << logC */
+  int32_t logC;      /* columns per streamed chunk = 1 << (logC & 0xff); bit 8: K1 streams
+                        the columns through ONE buffer (twice the columns, half the G) */
   int32_t log2G;     /* merge-path segments per pair = 1 << log2G */
   int32_t smem_mode; /* 1: K1 shared-memory tiles, 2: K1r one resident long row,
                         0: K1g one lane per pair from L1/L2 (exact mode, long rows) */

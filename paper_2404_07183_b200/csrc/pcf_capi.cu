@@ -1,6 +1,7 @@
 // C-ABI layer: argument checking, error text, the tile planner and the host-buffer
 // mirrors of the reference kernel module.  No exceptions cross this boundary.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 #include <algorithm>
@@ -115,6 +116,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   auto group_recs = [&](int64_t r) { return (int64_t)GW * sizes[r]; };  // r: first row of a group
   const int T = kTileThreads;
   constexpr int64_t kK1rMinRecs = 1024;
+  static const int kSingleMinLogG = getenv("PCF_SINGLE_MIN_LOG2G") ? atoi(getenv("PCF_SINGLE_MIN_LOG2G")) : 3;
   std::vector<pcf_work_item> runs[3];  // by kernel: K1 (mode 1), K1r (2), K1g (0)
   int64_t need_max = 0, k1r_need = 0;
   if (max_cols < 1) max_cols = 1 << 30;
@@ -145,6 +147,22 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     }
     const bool smem = best_logRG >= 0 && (r0 % GW) == 0;
     int rows, logC, logG;
+    bool single = false;
+    if (smem && best_logG >= kSingleMinLogG) {
+      // long rows: G >= 16 merge-path segments of a few dozen steps each.  A single
+      // column buffer of twice the columns halves G (half the co-rank searches and
+      // partial sums per cell) at the price of one exposed chunk load per chunk.
+      const int64_t rows_b = group_recs(r0) * RB + (best_logRG ? group_recs(r0 + GW) * RB : 0);
+      const int64_t C2 = (int64_t)1 << (best_logC + 1);
+      const int64_t c0 = r0 + 1, ce = std::min<int64_t>(c0 + C2, M);
+      const int64_t need1 = al(rows_b) + al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
+      if (need1 <= smem_budget) {
+        single = true;
+        best_logC += 1;
+        best_logG -= 1;
+        best_need = need1;
+      }
+    }
     if (smem) {
       rows = GW << best_logRG;
       logC = best_logC;
@@ -181,7 +199,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       w.nrows = (int32_t)Rr;
       w.col0 = (int32_t)c0;
       w.col1 = (int32_t)c1;
-      w.logC = logC;
+      w.logC = logC | (single ? 0x100 : 0);
       w.log2G = logG;
       w.smem_mode = mode;
       const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;

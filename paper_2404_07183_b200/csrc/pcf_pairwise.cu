@@ -191,12 +191,16 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const int it = s_item;
     if (it >= n_items) break;
     const PcfWorkItem W = items[it];
+    // logC bit 8: single-buffered columns (one chunk of twice the columns in flight, half
+    // the merge-path segments; the planner picks it where G would otherwise be >= 16)
+    const int logC = W.logC & 0xff;
+    const bool single = (W.logC >> 8) & 1;
     const int logRG = W.nrows > GW ? 1 : 0;
-    const int RG = 1 << logRG, C = 1 << W.logC, log2G = W.log2G, G = 1 << log2G;
+    const int RG = 1 << logRG, C = 1 << logC, log2G = W.log2G, G = 1 << log2G;
     const int rg0 = W.row0 >> LOGGW;
     const int64_t rbase = goff[rg0];
     const uint32_t row_bytes = (uint32_t)((goff[rg0 + RG] - rbase) * sizeof(RT));
-    const int nchunk = (W.col1 - W.col0 + C - 1) >> W.logC;
+    const int nchunk = (W.col1 - W.col0 + C - 1) >> logC;
     const int c_first_end = min(W.col0 + C, W.col1);
     const uint32_t col_cap =
         (uint32_t)((cend(c_first_end) - cstart(W.col0)) * sizeof(RT)) + 16u;
@@ -204,27 +208,32 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const uint32_t col_al = (col_cap + 127u) & ~127u;
     unsigned char* rowbuf = smem;
     unsigned char* colbase = smem + row_al;  // column buffer k at colbase + k * col_al
-    double* red = reinterpret_cast<double*>(smem + row_al + 2 * col_al);  // [2][512] partials
-    double* redh = red + 2 * kTileThreads;                                 // [2][pairs] tails
+    const int ncb = single ? 1 : 2;  // column buffers
+    double* red = reinterpret_cast<double*>(smem + row_al + ncb * col_al);  // [2][512] partials
+    double* redh = red + 2 * kTileThreads;                                   // [2][pairs] tails
+    // issue chunk c into its column buffer (thread 0)
+    auto issue = [&](int c) {
+      const int cb = W.col0 + (c << logC), ce = min(cb + C, W.col1);
+      const int64_t r0 = cstart(cb);
+      const uint32_t nb = (uint32_t)((cend(ce) - r0) * sizeof(RT));
+      const int kb = single ? 0 : (c & 1);
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[1 + kb], nb);
+      bulk_g2s(colbase + kb * col_al, recs + r0, nb, &bars[1 + kb]);
+    };
 
     if (tid == 0) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], row_bytes);
       bulk_g2s(rowbuf, recsg + rbase, row_bytes, &bars[0]);
-      for (int c = 0; c < 2 && c < nchunk; ++c) {
-        const int cb = W.col0 + (c << W.logC), ce = min(cb + C, W.col1);
-        const int64_t r0 = cstart(cb);
-        const uint32_t nb = (uint32_t)((cend(ce) - r0) * sizeof(RT));
-        mbar_arrive_expect_tx(&bars[1 + c], nb);
-        bulk_g2s(colbase + c * col_al, recs + r0, nb, &bars[1 + c]);
-      }
+      for (int c = 0; c < ncb && c < nchunk; ++c) issue(c);
     }
     // lane -> (row slot u, row group rho, column cc, segment g); fixed for the item
     const int u = tid & (GW - 1);
     const int Q = tid >> LOGGW;
     const int rho = Q & (RG - 1);
     const int cc = (Q >> logRG) & (C - 1);
-    const int g = Q >> (logRG + W.logC);
+    const int g = Q >> (logRG + logC);
     const int ps = W.row0 + GW * rho + u;
     const bool row_ok = ps < M;
     int nf = 0;
@@ -240,14 +249,15 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     ph_row ^= 1u;
 
     for (int c = 0; c < nchunk; ++c) {
-      const int buf = c & 1;
-      const int cb = W.col0 + (c << W.logC);
+      const int buf = c & 1;                 // partials buffer (alternates every chunk)
+      const int kb = single ? 0 : buf;       // column buffer
+      const int cb = W.col0 + (c << logC);
       const int ce = min(cb + C, W.col1);
       const int qs = cb + cc;
       const bool ok = row_ok && qs < ce && qs > ps;
-      mbar_wait(&bars[1 + buf], ph_col[buf]);
-      ph_col[buf] ^= 1u;
-      const RT* Gv = reinterpret_cast<const RT*>(colbase + buf * col_al);
+      mbar_wait(&bars[1 + kb], ph_col[kb]);
+      ph_col[kb] ^= 1u;
+      const RT* Gv = reinterpret_cast<const RT*>(colbase + kb * col_al);
       double acc = 0.0, hl = 0.0;
       if (ok) {
         const int ng = (int)(soff[qs + 1] - soff[qs]);
@@ -257,11 +267,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       }
       if (G == 1) {
         if (ok) finish_entry<BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
-        __syncthreads();  // buffer `buf` is free again
+        __syncthreads();  // column buffer `kb` is free again
+        if (tid == 0 && c + ncb < nchunk) issue(c + ncb);
       } else {
         red[buf * kTileThreads + g * npairs + pair_id] = acc;  // segment-major: no conflicts
         if (g == 0) redh[buf * kTileThreads + pair_id] = hl;
-        __syncthreads();  // partials visible, buffer `buf` free again
+        __syncthreads();  // partials visible, column buffer `kb` free again
+        if (tid == 0 && c + ncb < nchunk) issue(c + ncb);  // before finishing: keep TMA busy
         if (tid < npairs) {
           const int pu = tid & (GW - 1), prho = (tid >> LOGGW) & (RG - 1);
           const int pcc = tid >> (LOGGW + logRG);
@@ -274,14 +286,6 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                                         perm[pps], perm[pqs], out, ld, M, err);
           }
         }
-      }
-      if (tid == 0 && c + 2 < nchunk) {
-        const int nb0 = W.col0 + ((c + 2) << W.logC), ne = min(nb0 + C, W.col1);
-        const int64_t r0 = cstart(nb0);
-        const uint32_t nb = (uint32_t)((cend(ne) - r0) * sizeof(RT));
-        fence_proxy_async();
-        mbar_arrive_expect_tx(&bars[1 + buf], nb);
-        bulk_g2s(colbase + buf * col_al, recs + r0, nb, &bars[1 + buf]);
       }
     }
     __syncthreads();  // all finishers done before the next item reuses shared memory
