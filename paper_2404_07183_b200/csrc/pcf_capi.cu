@@ -116,7 +116,11 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   auto group_recs = [&](int64_t r) { return (int64_t)GW * sizes[r]; };  // r: first row of a group
   const int T = kTileThreads;
   constexpr int64_t kK1rMinRecs = 1024;
-  static const int kSingleMinLogG = getenv("PCF_SINGLE_MIN_LOG2G") ? atoi(getenv("PCF_SINGLE_MIN_LOG2G")) : 3;
+  static const int kSingleMinLogG =
+      getenv("PCF_SINGLE_MIN_LOG2G") ? atoi(getenv("PCF_SINGLE_MIN_LOG2G")) : 3;
+  // largest G accepted for single-buffered K1 on rows whose group misses double buffering
+  static const int kSingleFallbackLogG =
+      getenv("PCF_SINGLE_FALLBACK_LOG2G") ? atoi(getenv("PCF_SINGLE_FALLBACK_LOG2G")) : -1;
   std::vector<pcf_work_item> runs[3];  // by kernel: K1 (mode 1), K1r (2), K1g (0)
   int64_t need_max = 0, k1r_need = 0;
   if (max_cols < 1) max_cols = 1 << 30;
@@ -145,10 +149,29 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
         break;  // larger logC with this RG already failed or this one fits; keep smallest G
       }
     }
+    bool single = false;
+    if (best_logRG < 0 && kSingleFallbackLogG >= 0 && (r0 % GW) == 0) {
+      // the 8-row group fits only with ONE column buffer: K1 single-buffered at the
+      // largest column count that fits (instead of K1r / K1g)
+      const int64_t rows_b = group_recs(r0) * RB;
+      for (int lc = LOGU; lc >= 0; --lc) {
+        const int lg = LOGU - lc;
+        if (lg > max_log2G || lg > kSingleFallbackLogG) break;
+        const int64_t c0 = r0 + 1, ce = std::min<int64_t>(c0 + ((int64_t)1 << lc), M);
+        const int64_t need1 = al(rows_b) + al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
+        if (need1 <= smem_budget) {
+          best_logRG = 0;
+          best_logC = lc;
+          best_logG = lg;
+          best_need = need1;
+          single = true;
+          break;
+        }
+      }
+    }
     const bool smem = best_logRG >= 0 && (r0 % GW) == 0;
     int rows, logC, logG;
-    bool single = false;
-    if (smem && best_logG >= kSingleMinLogG) {
+    if (smem && !single && best_logG >= kSingleMinLogG) {
       // long rows: G >= 16 merge-path segments of a few dozen steps each.  A single
       // column buffer of twice the columns halves G (half the co-rank searches and
       // partial sums per cell) at the price of one exposed chunk load per chunk.
