@@ -119,10 +119,36 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   static const int kSingleMinLogG =
       getenv("PCF_SINGLE_MIN_LOG2G") ? atoi(getenv("PCF_SINGLE_MIN_LOG2G")) : 3;
   // largest G accepted for single-buffered K1 on rows whose group misses double buffering
+  static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
   static const int kSingleFallbackLogG =
       getenv("PCF_SINGLE_FALLBACK_LOG2G") ? atoi(getenv("PCF_SINGLE_FALLBACK_LOG2G")) : -1;
-  std::vector<pcf_work_item> runs[3];  // by kernel: K1 (mode 1), K1r (2), K1g (0)
-  int64_t need_max = 0, k1r_need = 0;
+  std::vector<pcf_work_item> runs[4];  // by kernel: K1 (mode 1), K1c (3), K1r (2), K1g (0)
+  int64_t need_max = 0, k1r_need = 0, k1c_need = 0;
+  const int64_t n_groups = (M + GW - 1) / GW;
+  // K1c (one long row resident, interleaved column groups streamed): the best config for a
+  // column range starting at group ks -- largest CG (fewest segments) that fits, double
+  // buffered if possible.  Returns false if not even one group fits.
+  auto k1c_config = [&](int64_t r, int64_t ks, int* lcg, int* lg, bool* one, int64_t* need) {
+    const int64_t row_need = al((sizes[r] + 4) * RB + 16);
+    for (int l = LOGU; l >= 0; --l) {
+      const int g = LOGU - l;
+      if (g > max_log2G) break;
+      const int64_t ke = std::min<int64_t>(ks + ((int64_t)1 << l), n_groups);
+      int64_t chunk = 0;
+      for (int64_t k = ks; k < ke; ++k) chunk += group_recs(GW * k) * RB;
+      for (int nb = 2; nb >= 1; --nb) {
+        const int64_t nd = row_need + nb * al(chunk + 16) + kRedBytes;
+        if (nd <= smem_budget) {
+          *lcg = l;
+          *lg = g;
+          *one = nb == 1;
+          *need = nd;
+          return true;
+        }
+      }
+    }
+    return false;
+  };
   if (max_cols < 1) max_cols = 1 << 30;
   int64_t r0 = 0;
   while (r0 < M - 1) {
@@ -207,16 +233,52 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       logC = 0;
       while ((rows << (logC + 1)) <= P) ++logC;
     }
-    const int mode = smem ? 1 : (rows == 1 ? 2 : 0);
+    int mode = smem ? 1 : (rows == 1 ? 2 : 0);
     int64_t Rr = std::min<int64_t>(rows, M - r0);
+    int64_t c_split = M;  // columns >= c_split of this row go to K1c
+    if (mode == 2 && kK1cEnabled) {
+      // the first column group small enough for K1c (group sizes fall along the sort)
+      int64_t lo = (r0 + 1) / GW, hi = n_groups;
+      int lcg, lg;
+      bool one;
+      int64_t nd;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (k1c_config(r0, mid, &lcg, &lg, &one, &nd)) hi = mid;
+        else lo = mid + 1;
+      }
+      if (lo < n_groups) {
+        c_split = std::max<int64_t>(r0 + 1, lo * GW);
+        // items of about max_cols columns, each with the config of its own first group
+        // (columns shorten along the sort, so later items stage more groups per chunk)
+        const int64_t span_c = std::max<int64_t>(GW, (max_cols / GW) * GW);
+        for (int64_t c0 = c_split; c0 < M; c0 = ((c0 / GW) * GW) + span_c) {
+          const int64_t c1 = std::min<int64_t>(((c0 / GW) * GW) + span_c, M);
+          k1c_config(r0, c0 / GW, &lcg, &lg, &one, &nd);
+          k1c_need = std::max(k1c_need, nd);
+          pcf_work_item w;
+          w.row0 = (int32_t)r0;
+          w.nrows = 1;
+          w.col0 = (int32_t)c0;
+          w.col1 = (int32_t)c1;
+          w.logC = lcg | (one ? 0x100 : 0);
+          w.log2G = lg;
+          w.smem_mode = 3;
+          const double cells = (double)(S[c1] - S[c0]) + (double)(c1 - c0) * sizes[r0];
+          w.cost_hi = (int32_t)std::min(2.0e9, cells / 1048576.0);
+          runs[1].push_back(w);
+        }
+      }
+    }
+    const int64_t c_end = mode == 2 ? c_split : M;
     // rows outside K1 stop at the next group boundary so that K1 can resume on an
     // aligned interleaved group
     if (!smem && (r0 % GW) != 0) Rr = std::min<int64_t>(Rr, GW - r0 % GW);
     const int C = 1 << logC;
     const int64_t span = std::max<int64_t>(C, (max_cols / C) * C);
     const int64_t rows_pts = S[r0 + Rr] - S[r0];
-    for (int64_t c0 = r0 + 1; c0 < M; c0 += span) {
-      const int64_t c1 = std::min<int64_t>(c0 + span, M);
+    for (int64_t c0 = r0 + 1; c0 < c_end; c0 += span) {
+      const int64_t c1 = std::min<int64_t>(c0 + span, c_end);
       pcf_work_item w;
       w.row0 = (int32_t)r0;
       w.nrows = (int32_t)Rr;
@@ -227,7 +289,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       w.smem_mode = mode;
       const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;
       w.cost_hi = (int32_t)std::min(2.0e9, cells / 1048576.0);
-      runs[mode == 1 ? 0 : (mode == 2 ? 1 : 2)].push_back(w);
+      runs[mode == 1 ? 0 : (mode == 2 ? 2 : 3)].push_back(w);
     }
     if (smem) need_max = std::max(need_max, best_need);
     r0 += Rr;
@@ -236,9 +298,10 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     return x.cost_hi > y.cost_hi;
   };
   for (auto& r : runs) std::stable_sort(r.begin(), r.end(), by_cost);
-  const int64_t total = (int64_t)(runs[0].size() + runs[1].size() + runs[2].size());
+  const int64_t total =
+      (int64_t)(runs[0].size() + runs[1].size() + runs[2].size() + runs[3].size());
   *n_items = total;
-  if (smem_bytes) *smem_bytes = (int32_t)std::max(need_max, k1r_need);
+  if (smem_bytes) *smem_bytes = (int32_t)std::max(std::max(need_max, k1r_need), k1c_need);
   if (items) {
     if (cap < total) {
       set_error("pcf_plan_pairwise: capacity %lld < %lld items", (long long)cap, (long long)total);

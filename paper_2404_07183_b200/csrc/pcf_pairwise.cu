@@ -293,6 +293,131 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   }
 }
 
+// K1c: one long row resident, interleaved column groups streamed -- K1 with the roles
+// swapped, for rows too long for an 8-row group (c4's heavy tail).  A quarter-warp holds
+// the GW columns of one interleaved group (recsg, the layout K1 stages its row groups in)
+// against the row, so the column reads of a quarter hit GW distinct bank groups; only the
+// row reads (lanes at unrelated positions of one PCF) can conflict.  64 quarters = CG
+// groups per chunk x G merge-path segments; the groups stream through one or two shared
+// buffers by bulk copy like K1's columns, the row is staged once per item.  Segment
+// partials are added by one finishing thread per pair as in K1.
+template <int HK, bool BOUNDED, typename OutT, typename RT, int GW>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_fill_colgroups(const RT* __restrict__ recs, const RT* __restrict__ recsg,
+                     const int64_t* __restrict__ soff, const int64_t* __restrict__ goff,
+                     const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
+                     int n_items, int* __restrict__ counter, double p, double a, double b,
+                     int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
+                     unsigned long long* __restrict__ err,
+                     const int32_t* __restrict__ item_tag, int32_t* __restrict__ tag_done) {
+  constexpr int LOGGW = GW == 16 ? 4 : 3;
+  constexpr int CA = 16 / (int)sizeof(RT);
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[3];  // 0: row, 1/2: column-group buffers
+  __shared__ int s_item;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t ph_row = 0, ph_col[2] = {0u, 0u};
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= n_items) break;
+    const PcfWorkItem W = items[it];
+    const int logCG = W.logC & 0xff;
+    const bool single = (W.logC >> 8) & 1;
+    const int CG = 1 << logCG, log2G = W.log2G, G = 1 << log2G;
+    const int ps = W.row0;
+    const int nf = (int)(soff[ps + 1] - soff[ps]);
+    const int64_t oi = perm[ps];
+    const int64_t rlo = soff[ps] - soff[ps] % CA;
+    const int64_t rhi = (soff[ps + 1] + CA - 1) / CA * CA;
+    const uint32_t row_bytes = (uint32_t)((rhi - rlo) * sizeof(RT));
+    const int gk0 = W.col0 >> LOGGW, gk1 = (W.col1 + GW - 1) >> LOGGW;
+    const int nchunk = (gk1 - gk0 + CG - 1) >> logCG;
+    const uint32_t col_cap =
+        (uint32_t)((goff[min(gk0 + CG, gk1)] - goff[gk0]) * sizeof(RT));
+    const uint32_t row_al = (row_bytes + 127u) & ~127u;
+    const uint32_t col_al = (col_cap + 127u) & ~127u;
+    const int ncb = single ? 1 : 2;
+    unsigned char* rowbuf = smem;
+    unsigned char* colbase = smem + row_al;
+    double* red = reinterpret_cast<double*>(smem + row_al + ncb * col_al);  // [2][512] partials
+    double* redh = red + 2 * kTileThreads;                                   // [2][pairs] tails
+    auto issue = [&](int c) {
+      const int kb0 = gk0 + (c << logCG), kb1 = min(kb0 + CG, gk1);
+      const uint32_t nb = (uint32_t)((goff[kb1] - goff[kb0]) * sizeof(RT));
+      const int kb = single ? 0 : (c & 1);
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[1 + kb], nb);
+      bulk_g2s(colbase + kb * col_al, recsg + goff[kb0], nb, &bars[1 + kb]);
+    };
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[0], row_bytes);
+      bulk_g2s(rowbuf, recs + rlo, row_bytes, &bars[0]);
+      for (int c = 0; c < ncb && c < nchunk; ++c) issue(c);
+    }
+    const int u = tid & (GW - 1);
+    const int Q = tid >> LOGGW;
+    const int cg = Q & (CG - 1);
+    const int g = Q >> logCG;
+    const RT* F = reinterpret_cast<const RT*>(rowbuf) + (soff[ps] - rlo);
+    const int pair_id = cg * GW + u;
+    const int npairs = GW * CG;
+    mbar_wait(&bars[0], ph_row);
+    ph_row ^= 1u;
+    for (int c = 0; c < nchunk; ++c) {
+      const int buf = c & 1;
+      const int kb = single ? 0 : buf;
+      const int kbase = gk0 + (c << logCG);
+      const int k = kbase + cg;
+      const int64_t qs = (int64_t)k * GW + u;
+      const bool ok = k < gk1 && qs >= W.col0 && qs < W.col1 && qs > ps && qs < M;
+      mbar_wait(&bars[1 + kb], ph_col[kb]);
+      ph_col[kb] ^= 1u;
+      double acc = 0.0, hl = 0.0;
+      if (ok) {
+        const RT* Gv = reinterpret_cast<const RT*>(colbase + kb * col_al) +
+                       (goff[k] - goff[kbase]) + u;
+        const int ng = (int)(soff[qs + 1] - soff[qs]);
+        acc = lane_walk<HK, BOUNDED, 1, GW, RT>(F, nf, Gv, ng, g, log2G, p, a, b);
+        if (!BOUNDED) hl = hval<HK>(F[nf - 1].v, Gv[(ng - 1) * GW].v, p);
+      }
+      if (G == 1) {
+        if (ok) finish_entry<BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
+        __syncthreads();
+        if (tid == 0 && c + ncb < nchunk) issue(c + ncb);
+      } else {
+        red[buf * kTileThreads + g * npairs + pair_id] = acc;
+        if (g == 0) redh[buf * kTileThreads + pair_id] = hl;
+        __syncthreads();
+        if (tid == 0 && c + ncb < nchunk) issue(c + ncb);
+        if (tid < npairs) {
+          const int pu = tid & (GW - 1), pcg = tid >> LOGGW;
+          const int pk = kbase + pcg;
+          const int64_t pqs = (int64_t)pk * GW + pu;
+          if (pk < gk1 && pqs >= W.col0 && pqs < W.col1 && pqs > ps && pqs < M) {
+            const double* r = red + buf * kTileThreads + tid;
+            double sacc = r[0];
+            for (int kk = 1; kk < G; ++kk) sacc = __dadd_rn(sacc, r[kk * npairs]);
+            finish_entry<BOUNDED, OutT>(sacc, redh[buf * kTileThreads + tid], p, apply_root,
+                                        oi, perm[pqs], out, ld, M, err);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tag_done && tid == 0) signal_item(item_tag, tag_done, it);
+  }
+}
+
 // K1g: tiles whose PCFs are too long to stage; operands read straight from the
 // contiguous records through L1/L2.  R x C pairs per pass, G lanes per pair in one warp
 // (butterfly reduction).
@@ -666,6 +791,25 @@ static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
       kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
           (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
           A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
+    }
+  } else if (A.smem_mode == 3) {
+    cudaError_t e;
+    if (A.rec_bytes == 8) {
+      auto kern = k_fill_colgroups<HK, BOUNDED, OutT, Rec32, 16>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+          (const Rec32*)A.recs, (const Rec32*)A.recs8, A.soff, A.goff8, A.perm, A.items,
+          A.n_items, A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err,
+          A.item_tag, A.tag_done);
+    } else {
+      auto kern = k_fill_colgroups<HK, BOUNDED, OutT, Rec, 8>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+          (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
+          A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag,
+          A.tag_done);
     }
   } else if (A.smem_mode == 2) {
     const size_t sm = (size_t)A.smem_bytes;

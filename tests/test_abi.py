@@ -95,6 +95,14 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
             assert al(rows_b) + nbuf * al(col_b) + 4 * 512 * 8 <= smem <= 220 * 1024
             if single:  # only where the double-buffered split would be G >= 8
                 assert G >= 4
+        elif mode == 3:  # K1c: one resident row x interleaved column groups (CG x G units)
+            assert nrows == 1 and C * G == units
+            gs = [gw * sizes[gw * k] * rec_bytes for k in range(col0 // gw,
+                                                               min((col0 // gw) + C, (M + gw - 1) // gw))]
+            al = lambda x: (x + 127) // 128 * 128  # noqa: E731
+            nbuf = 1 if single else 2
+            assert al((sizes[row0] + 4) * rec_bytes + 16) + nbuf * al(sum(gs) + 16) + 4 * 512 * 8 \
+                <= smem <= 220 * 1024
         elif mode == 2:  # K1r: one resident row, C columns x G segments
             assert nrows == 1 and C * G == threads and G <= 32
             assert (sizes[row0] * rec_bytes + 127) // 128 * 128 <= smem <= 220 * 1024
@@ -111,11 +119,11 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
     iu = np.triu_indices(M, 1)
     assert (seen[iu] == 1).all()
     assert seen.sum() == M * (M - 1) // 2
-    for m in (1, 2, 0):
+    for m in (1, 3, 2, 0):
         costs = items[items[:, 6] == m][:, 7]
         assert (np.diff(costs) <= 0).all()  # LPT order within each kernel's run
     runs = [m for k, m in enumerate(items[:, 6]) if k == 0 or items[k - 1, 6] != m]
-    assert runs == [m for m in (1, 2, 0) if m in runs]  # one contiguous run per kernel
+    assert runs == [m for m in (1, 3, 2, 0) if m in runs]  # one contiguous run per kernel
 
 
 def test_planner_rejects_unsorted():

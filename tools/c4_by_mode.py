@@ -15,7 +15,7 @@ t, v, off = dg.pack_matrices(dg.ecc_like_collection(M))
 coll = DeviceCollection(t, v, off)
 dev_items, host, smem = coll.plan()
 out = torch.empty((M, M), dtype=torch.float64, device="cuda")
-for mode, name in ((1, "K1"), (2, "K1r"), (0, "K1g")):
+for mode, name in ((1, "K1"), (3, "K1c"), (2, "K1r"), (0, "K1g")):
     sel = host[host[:, 6] == mode]
     if sel.shape[0] == 0:
         continue
