@@ -150,6 +150,16 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     return false;
   };
   if (max_cols < 1) max_cols = 1 << 30;
+  {
+    // small collections: cut the column ranges finer so the persistent kernels see
+    // ~8 items per SM (c1's 1000 PCFs are 63 row blocks: one item each would leave
+    // 85 of 148 SMs idle)
+    const double target = 8.0 * 148.0;
+    const double want = (double)(M / 8 + 1) * (double)M / (2.0 * target);
+    int64_t mc = 64;
+    while (mc < want && mc < max_cols) mc <<= 1;
+    max_cols = std::min<int64_t>(max_cols, mc);
+  }
   int64_t r0 = 0;
   while (r0 < M - 1) {
     int best_logRG = -1, best_logC = 0, best_logG = 99;
