@@ -182,6 +182,40 @@ def cpu_reference_sample(t, v, off, seconds, threads=None):
     return state["pairs"] / dt, state["cells"] / dt, kind, threads, desc
 
 
+def reference_rows_parity(t, v, off, gpu_rows):
+    """The e2e (host) result's sampled rows against the reference's own kernel
+    (oracle/_ref; the C port if the reference could not be built), one row per call:
+    fill_block(i, i + 1) into an O(M) aliasing sink leaves D[i, i+1:] in buf[i+1:]
+    (SURVEY.md 8d).  North-star tolerance: relative 1e-12."""
+    import concurrent.futures
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from numpy.lib.stride_tricks import as_strided
+
+    M = off.shape[0] - 1
+    K = O.load_reference_kernel()
+    packed = (np.ascontiguousarray(t), np.ascontiguousarray(v), np.ascontiguousarray(off))
+
+    def ref_row(i):
+        if K is None:
+            return O.Oracle().row(packed[0], packed[1], packed[2], i)
+        buf = np.zeros(M)
+        K.fill_block(packed, i, i + 1, 0, 1.0, True, False, 0.0, math.inf,
+                     as_strided(buf, shape=(M, M), strides=(0, 8)))
+        return buf
+
+    worst, rows = 0.0, sorted(gpu_rows)
+    with concurrent.futures.ThreadPoolExecutor(len(rows)) as ex:
+        for i, ref in zip(rows, ex.map(ref_row, rows)):
+            got, want = gpu_rows[i][i + 1:], ref[i + 1:]
+            worst = max(worst, float(np.max(np.abs(got - want) /
+                                            np.maximum(np.abs(want), 1e-300))))
+    return {"rows": rows, "columns_per_row": "all j > i", "max_rel": worst, "tol": 1e-12,
+            "ok": worst < 1e-12, "checked": "e2e host result (pcf_matrix_host)",
+            "against": "reference _sweepkern.fill_block" if K is not None else "C port"}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -331,10 +365,13 @@ def run_ours(args):
         lib.pcf_release_workspace()
 
     cpu = None
+    gpu_rows = e2e.pop("_rows", None) if e2e else None
     if rank == 0 and world == 1 and not args.no_cpu:
         pps, cps, kind, cores, desc = cpu_reference_sample(t, v, off, args.cpu_seconds)
         cpu = {"value": pps, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc,
                "cells_per_s": cps, "extrapolated_full_matrix_s": cells / cps}
+        if gpu_rows:
+            cpu["parity"] = reference_rows_parity(t, v, off, gpu_rows)
 
     if rank == 0:
         line = {
@@ -476,8 +513,14 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         ms = float(tt.item())
-    return {"value": pairs * k / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": bi,
-            "d2h_bytes_per_step": bo, "ms_per_step": ms / k, "steps": k, "path": path}
+    res = {"value": pairs * k / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": bi,
+           "d2h_bytes_per_step": bo, "ms_per_step": ms / k, "steps": k, "path": path}
+    if rank == 0:
+        # a few rows of the host result, checked against the reference kernel by the CPU
+        # leg (the only place bench.py runs oracle/)
+        res["_rows"] = {int(i): host_out[int(i)].numpy().copy()
+                        for i in sorted({1, M // 3, (2 * M) // 3, M - 2}) if 0 <= i < M - 1}
+    return res
 
 
 def _build_collection(coll, dt, dv, do, off_host, dev):
