@@ -35,6 +35,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PCF pair-integrals/sec (100k-PCF L1 distance matrix)"
+# collectives backend: nccl (one GPU per rank); PCF_BENCH_BACKEND=gloo runs the same
+# multi-rank logic with host-side collectives, e.g. two ranks on one GPU for testing
+BACKEND = os.environ.get("PCF_BENCH_BACKEND", "nccl")
 UNIT = "pair-integrals/s"
 FLOPS_PER_CELL_L1 = 4  # |vf - vg|, tn - t, mul, add
 
@@ -272,9 +275,14 @@ def run_ours(args):
                                               mode_runs, new_err, partition_items)
 
     world, rank, local = dist_env()
+    if BACKEND != "nccl":  # ranks may share a GPU
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # test plumbing: several ranks sharing one GPU (NCCL refuses that)
+            tdist.init_process_group("gloo")
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     lib = _native.load()
@@ -333,7 +341,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev if BACKEND == "nccl" else "cpu")
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         tdist.barrier()
         ms = float(tt.item())
@@ -385,7 +393,8 @@ def run_ours(args):
                 "M": M, "pairs": pairs, "cells": cells,
                 "mode": "exact (1 lane/pair)" if args.exact else "fast (merge-path G lanes/pair)",
                 "parallelism": f"tile-queue split over {world} GPU(s)",
-                "l2": "no flush needed: 0.81 GB input records + 80 GB output per step >> 126 MB L2",
+                "l2": f"no flush needed: {16 * int(off[-1]) / 1e9:.2f} GB input records + "
+                      f"{8 * M * M / 1e9:.1f} GB output per step >> 126 MB L2",
                 "work_items": int(host_items.shape[0]), "smem_bytes": smem,
             },
             "clocks": clk.summary(),
@@ -490,7 +499,13 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
             items = (items_dev, host_items, smem)
         fill_pairwise(coll, 0, 1.0, True, False, out=out, items=items)
         if world > 1:
-            tdist.reduce(out, dst=0)
+            if BACKEND == "nccl":
+                tdist.reduce(out, dst=0)
+            else:
+                host = out.cpu()
+                tdist.reduce(host, dst=0)
+                if rank == 0:
+                    out.copy_(host)
         if rank == 0:
             host_out.copy_(out, non_blocking=True)
 
@@ -510,7 +525,7 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev if BACKEND == "nccl" else "cpu")
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         ms = float(tt.item())
     res = {"value": pairs * k / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": bi,
