@@ -520,8 +520,8 @@ __global__ void k_fix_offsets(const int64_t* __restrict__ off, const int64_t* __
 // bit for bit; the finalisation (k_scale_flag / k_std_flag with times) drops zero-width
 // pieces and then minimises, which is the reference's result (intermediate emission
 // never changes values, only which redundant points exist).
-template <typename T, int K>
-__global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
+template <typename T, int K, int MT>
+__global__ void __launch_bounds__(MT, (K == K_MOM ? 3 : 4) * 256 / MT)
     k_merge_level(const T* __restrict__ t, const void* __restrict__ v_,
                   const double* __restrict__ v2, const int64_t* __restrict__ off,
                   const int64_t* __restrict__ src, const int32_t* __restrict__ cnt,
@@ -532,7 +532,8 @@ __global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
   const VT* __restrict__ v = reinterpret_cast<const VT*>(v_);
   VT* __restrict__ v_out = reinterpret_cast<VT*>(v_out_);
   constexpr bool MOM = (K == K_MOM);
-  constexpr int WCAP = wcap<T>();
+  constexpr int MLT = MT * LPT;  // candidate positions per tile
+  constexpr int WCAP = MLT + (4 + 4 * (16 / (int)sizeof(T) - 1)) * MAXSEG;
   constexpr int U = 16 / (int)sizeof(T);
 
   __shared__ Seg seg[MAXSEG];
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
   T* s_t = reinterpret_cast<T*>(dyn + WCAP * sizeof(VT) + (MOM ? WCAP * sizeof(double) : 0));
   __shared__ uint64_t s_bar;
   __shared__ int64_t s_next_node, s_round_end;
-  typedef cub::BlockScan<int, LTH> Scan;
+  typedef cub::BlockScan<int, MT> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
 
   const int tid = threadIdx.x;
@@ -555,9 +556,9 @@ __global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
   __syncthreads();
   const int64_t tile = blockIdx.x;
   const int64_t ntot = off[src[nout - 1] + cnt[nout - 1]];
-  const int64_t e0 = tile * (int64_t)LT;
+  const int64_t e0 = tile * (int64_t)MLT;
   if (e0 >= ntot) return;
-  const int64_t e1 = min(e0 + (int64_t)LT, ntot);
+  const int64_t e1 = min(e0 + (int64_t)MLT, ntot);
   int64_t kr = tile_node[tile];
   int64_t rs = e0;
   while (rs < e1) {
@@ -786,11 +787,12 @@ template <typename T>
 __global__ void k_tile_part(const T* __restrict__ t, const int64_t* __restrict__ off,
                             const int64_t* __restrict__ src, const int32_t* __restrict__ cnt,
                             int64_t nout, int64_t ntot, int64_t ntiles,
-                            int64_t* __restrict__ tile_node, int64_t* __restrict__ tile_i) {
+                            int64_t* __restrict__ tile_node, int64_t* __restrict__ tile_i,
+                            int64_t lt = LT) {
   ntot = off[src[nout - 1] + cnt[nout - 1]];  // live point count (ntot: upper bound)
   for (int64_t tl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tl <= ntiles;
        tl += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = min(tl * (int64_t)LT, ntot);
+    const int64_t e = min(tl * lt, ntot);
     int64_t lo = 0, hi = nout - 1;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
@@ -930,7 +932,9 @@ int pcf_tree_merge_level(int kind, int is_f32, const void* t_dev, const void* v_
   const int og = (int)((nout + 1 + 255) / 256 < 4096 ? (nout + 1 + 255) / 256 : 4096);
   k_merge_offsets<<<og, 256, 0, s>>>(off_dev, src_dev, cnt_dev, nout, off_out_dev);
   if (ntot <= 0) return PCF_OK;
-  const int64_t ntiles = (ntot + LT - 1) / LT;
+  constexpr int MT = 256;  // threads per merge tile (MT * LPT positions; 512 measured slower)
+  constexpr int64_t MLT = (int64_t)MT * LPT;
+  const int64_t ntiles = (ntot + MLT - 1) / MLT;
   int64_t need = 0;
   pcf_tree_level_workspace(ntot, &need);
   if (ws_bytes < need) {
@@ -945,12 +949,13 @@ int pcf_tree_merge_level(int kind, int is_f32, const void* t_dev, const void* v_
 #define PCF_ML(T, K)                                                                          \
   do {                                                                                        \
     typedef typename std::conditional<K == K_MOM, double, T>::type VT_;                      \
-    const int dsm = wcap<T>() * (int)(sizeof(VT_) + sizeof(T) + (K == K_MOM ? sizeof(double) : 0)); \
+    const int wc = (int)MLT + (4 + 4 * (16 / (int)sizeof(T) - 1)) * MAXSEG;                 \
+    const int dsm = wc * (int)(sizeof(VT_) + sizeof(T) + (K == K_MOM ? sizeof(double) : 0)); \
     k_tile_part<T><<<pg, 256, 0, s>>>((const T*)t_dev, off_dev, src_dev, cnt_dev, nout, ntot, \
-                                      ntiles, tile_node, tile_i);                             \
-    cudaFuncSetAttribute(k_merge_level<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                      ntiles, tile_node, tile_i, MLT);                        \
+    cudaFuncSetAttribute(k_merge_level<T, K, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          dsm);                                                                \
-    k_merge_level<T, K><<<grid, LTH, dsm, s>>>((const T*)t_dev, v_dev, v2_dev, off_dev,       \
+    k_merge_level<T, K, MT><<<grid, MT, dsm, s>>>((const T*)t_dev, v_dev, v2_dev, off_dev,    \
                                                src_dev, cnt_dev, leaves_dev, nout, tile_node, \
                                                tile_i, (T*)t_out_dev, v_out_dev, v2_out_dev); \
   } while (0)
