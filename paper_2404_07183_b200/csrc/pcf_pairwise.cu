@@ -83,16 +83,22 @@ __device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
     ST tt = tx; tx = ty; ty = tt;
     tt = vx; vx = vy; vy = tt;
   }
+  // The current cell's integrand h(v_X, v_Y) is carried instead of v_X: after X advances
+  // to (nt, nv) the next cell's integrand is h(nv, v_Y) whether or not the roles swap
+  // (a swap makes the old Y the new X and nv the new Y; h is symmetric bit for bit), so
+  // v_X never needs selecting.
   double acc = 0.0;
+  double hc = hval<HK>((double)vx, (double)vy, p);
   const int steps = d1 - d0;
 #pragma unroll 4
   for (int s = 0; s < steps; ++s) {
     double tn = (double)tx;
     if (BOUNDED) tn = fmin(tn, b);
-    acc = __dadd_rn(acc, __dmul_rn(hval<HK>((double)vx, (double)vy, p), __dsub_rn(tn, t)));
+    acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(tn, t)));
     t = tn;
     xp += xs;
     const ST nt = xp->t, nv = xp->v;
+    hc = hval<HK>((double)nv, (double)vy, p);
     const bool sw = nt > ty;
     const RT* __restrict__ np = sw ? yp : xp;
     yp = sw ? xp : yp;
@@ -103,12 +109,11 @@ __device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
       xs = ns;
     }
     tx = sw ? ty : nt;
-    vx = sw ? vy : nv;
     ty = sw ? nt : ty;
     vy = sw ? nv : vy;
   }
   if (BOUNDED && (lane == (1 << log2G) - 1)) {
-    acc = __dadd_rn(acc, __dmul_rn(hval<HK>((double)vx, (double)vy, p), __dsub_rn(b, t)));
+    acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(b, t)));
   }
   return acc;
 }
