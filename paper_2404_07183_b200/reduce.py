@@ -155,6 +155,32 @@ def _plan_levels(seg_nodes, leaves0=None, moments=False):
 
 
 _PLAN_CACHE = {}
+_SCRATCH = {}
+
+
+def _in_scratch(x):
+    if x is None:
+        return False
+    p = x.data_ptr()
+    for buf in _SCRATCH.values():
+        b = buf.data_ptr()
+        if b <= p < b + buf.numel() * buf.element_size():
+            return True
+    return False
+
+
+def _scratch(name, numel, dtype, dev):
+    """A cached device buffer of at least `numel` elements (grow-only, per name / dtype /
+    device); the caller uses the first `numel`.  Results never alias scratch: the tree's
+    output level is copied out by _finalize / to_pcfs before the next tree runs."""
+    torch = _torch()
+    key = (name, dtype, str(dev))
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < numel:
+        _SCRATCH.pop(key, None)
+        buf = torch.empty(max(int(numel), 1), dtype=dtype, device=dev)
+        _SCRATCH[key] = buf
+    return buf[:numel]
 
 
 def _device_plan(seg_nodes, leaves0, moments, dev):
@@ -195,15 +221,23 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
     plan, leaves_final, src_d, cnt_d, lv_d = _device_plan(seg_nodes, leaves0, moments, dev)
     if not plan:
         return level, leaves_final
+    if _in_scratch(level.t) or _in_scratch(level.v) or _in_scratch(level.m2):
+        # the input is a previous tree's output (scratch): copy it out before reuse
+        level = DeviceLevel(level.t.clone(), level.v.clone(), level.off.clone(), level.nnodes,
+                            level.ntot, level.is_f32,
+                            None if level.m2 is None else level.m2.clone())
     bound = max(level.ntot, 1)
     nb = _native.c_i64(0)
     lib.pcf_tree_level_workspace(bound, _native.ctypes.byref(nb))
-    ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=dev)
+    ws = _scratch("ws", max(nb.value, 256), torch.uint8, dev)
     kind = 4 if moments else int(op)
-    bufs = [(torch.empty(bound, dtype=level.t.dtype, device=dev),
-             torch.empty(bound, dtype=level.v.dtype, device=dev),
-             torch.empty(bound, dtype=torch.float64, device=dev) if moments else None)
-            for _ in range(2)]
+    # the level ping-pong buffers and the workspace come from a grow-only cache: a tree of
+    # 1e8 points needs ~5 GB of scratch, and re-allocating it per call from a fragmented
+    # caching allocator costs synchronising cudaFree/cudaMalloc rounds
+    bufs = [(_scratch(f"t{k}", bound, level.t.dtype, dev),
+             _scratch(f"v{k}", bound, level.v.dtype, dev),
+             _scratch(f"m{k}", bound, torch.float64, dev) if moments else None)
+            for k in range(2)]
     so = lo = 0
     cur_t, cur_v, cur_m2, cur_off = level.t, level.v, level.m2, level.off
     nout = level.nnodes
@@ -419,7 +453,10 @@ class ReductionAccumulator:
         off = torch.tensor([0, st.ntot, st.ntot + lvl.ntot], dtype=torch.int64,
                            device=t.device)
         pair = DeviceLevel(t, v, off, 2, st.ntot + lvl.ntot, self.dtype == np.float32)
-        self._state, _ = _run_tree(pair, [2], op=self._code)
+        out, _ = _run_tree(pair, [2], op=self._code)
+        # the tree's output lives in shared scratch: the state keeps its own copy
+        self._state = DeviceLevel(out.t[: out.ntot].clone(), out.v[: out.ntot].clone(),
+                                  out.off.clone(), 1, out.ntot, out.is_f32)
 
     def to_pcf(self) -> Pcf:
         """Snapshot the state as an immutable Pcf."""

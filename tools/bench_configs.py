@@ -208,4 +208,5 @@ def c5():
 if __name__ == "__main__":
     which = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c1", "c2", "c4", "c5"]
     for w in which:
+        torch.cuda.empty_cache()  # each config starts from a clean caching allocator
         globals()[w]()
