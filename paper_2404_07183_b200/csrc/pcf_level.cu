@@ -668,9 +668,14 @@ __global__ void __launch_bounds__(MT, (K == K_MOM ? 3 : 4) * 256 / MT)
     mbar_wait(&s_bar, bar_phase);
     bar_phase ^= 1u;
     __syncthreads();
-    // ---- walk: every candidate is written at its own position rs + p
+    // ---- walk: every candidate lands at its own position rs + p; values are collected in
+    //      registers and written out through shared memory as coalesced rows (thread-
+    //      strided global stores made the L1 the bottleneck of this kernel)
     const int p0 = tid * LPT;
     const int rlen = (int)(re - rs);
+    T o_t[LPT];
+    VT o_v[LPT];
+    double o_v2[LPT];
     if (p0 < rlen) {
       int sg;
       {
@@ -719,7 +724,6 @@ __global__ void __launch_bounds__(MT, (K == K_MOM ? 3 : 4) * 256 / MT)
         tbj = j < (int)g.nb ? pb_t[j] : TINF;
       };
       start((int)g.m0 + (p0 - seg_pos[sg]));
-      int64_t pos = rs + p0;
 #pragma unroll
       for (int q = 0; q < LPT; ++q) {
         const int p = p0 + q;
@@ -758,12 +762,31 @@ __global__ void __launch_bounds__(MT, (K == K_MOM ? 3 : 4) * 256 / MT)
             tai = takeA ? nxt : tai;
             tbj = takeA ? tbj : nxt;
           }
-          t_out[pos] = tt;
-          v_out[pos] = val;
-          if (MOM) v2_out[pos] = val2;
-          ++pos;
+          o_t[q] = tt;
+          o_v[q] = val;
+          if (MOM) o_v2[q] = val2;
         }
       }
+    }
+    __syncthreads();  // the staged windows are free: reuse them for the output rows
+    {
+      // element p at p + p / LPT (one pad slot per thread: 2-way bank conflicts at most)
+#pragma unroll
+      for (int q = 0; q < LPT; ++q) {
+        if (p0 + q < rlen) {
+          const int x = p0 + q + tid;
+          s_t[x] = o_t[q];
+          s_v[x] = o_v[q];
+          if (MOM) s_v2[x] = o_v2[q];
+        }
+      }
+    }
+    __syncthreads();
+    for (int x = tid; x < rlen; x += MT) {
+      const int y = x + x / LPT;
+      t_out[rs + x] = s_t[y];
+      v_out[rs + x] = s_v[y];
+      if (MOM) v2_out[rs + x] = s_v2[y];
     }
     rs = re;
     kr = s_next_node;
@@ -932,7 +955,7 @@ int pcf_tree_merge_level(int kind, int is_f32, const void* t_dev, const void* v_
   const int og = (int)((nout + 1 + 255) / 256 < 4096 ? (nout + 1 + 255) / 256 : 4096);
   k_merge_offsets<<<og, 256, 0, s>>>(off_dev, src_dev, cnt_dev, nout, off_out_dev);
   if (ntot <= 0) return PCF_OK;
-  constexpr int MT = 256;  // threads per merge tile (MT * LPT positions; 512 measured slower)
+  constexpr int MT = 256;  // threads per merge tile (MT * LPT positions; 128 and 512 measured slower)
   constexpr int64_t MLT = (int64_t)MT * LPT;
   const int64_t ntiles = (ntot + MLT - 1) / MLT;
   int64_t need = 0;
