@@ -473,18 +473,27 @@ __global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
   }
   __syncthreads();
   const int64_t out_base = s_excl;
-  // ---- 5. write the kept points
+  // ---- 5. write the kept points: through the (now free) window buffers so the global
+  //         stores are coalesced rows instead of per-thread strided runs
   if (!multi) {
     int r = 0;
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
       if ((my_kmask >> q) & 1u) {
-        const int64_t x = out_base + my_koff + r;
-        t_out[x] = o_t[q];
-        v_out[x] = o_v[q];
-        if (MOM) v2_out[x] = o_v2[q];
+        const int x = my_koff + r;
+        const int y = x + x / LPT;  // one pad slot per LPT: few bank conflicts
+        s_t[y] = o_t[q];
+        s_v[y] = o_v[q];
+        if (MOM) s_v2[y] = o_v2[q];
         ++r;
       }
+    }
+    __syncthreads();
+    for (int x = tid; x < kept_run; x += LTH) {
+      const int y = x + x / LPT;
+      t_out[out_base + x] = s_t[y];
+      v_out[out_base + x] = s_v[y];
+      if (MOM) v2_out[out_base + x] = s_v2[y];
     }
   } else {
     for (int x = tid; x < kept_run; x += LTH) {
