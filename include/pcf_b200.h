@@ -224,8 +224,8 @@ int pcf_compact(int is_f32, const void* st_dev, const void* sv_dev, const void* 
                 const int64_t* src_dev, int64_t nout, int64_t* pos_dev, void* temp_dev,
                 int64_t temp_bytes, void* t_out_dev, void* v_out_dev, void* v2_out_dev,
                 int64_t* off_out_dev, void* stream);
-/* Whole tree level, tiled two-pass (count -> tile scan -> write); replaces
- * merge + compact.  kind 0..3 = add/max/min/mul on v (the PCFs' kind); 4 = moments
+/* Whole tree level, tiled single pass (stage windows -> merge walk with reduce_pair's keep
+ * flags -> block scan -> decoupled look-back -> coalesced writes).  kind 0..3 = add/max/min/mul on v (the PCFs' kind); 4 = moments
  * (v = mean, v2 = M2, both float64; leaves_dev = leaf counts per input node).  Writes
  * t_out/v_out(/v2_out) and off_out[nout+1]; workspace from pcf_tree_level_workspace. */
 int pcf_tree_level_workspace(int64_t ntot, int64_t* bytes);

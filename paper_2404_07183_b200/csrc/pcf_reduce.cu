@@ -1,16 +1,10 @@
 // Reduction path helpers: compaction (scan + scatter) and the mean/std finalisation
 // (reduce.py:211-238, core.py:165-214).  The tree levels themselves are in pcf_level.cu.
 //
-// A level is a list of nodes (PCFs as SoA times/values + int64 offsets).  Output node k
-// merges input nodes src[k] and src[k]+1 (cnt[k] == 2) or passes src[k] through
-// (cnt[k] == 1, the reference's "No-Op passthrough").  Because output nodes consume
-// consecutive input nodes, the merged candidate sequence of output node k occupies
-// exactly the input positions [off[src[k]], off[src[k]+cnt[k]]): K5 writes one
-// candidate (time, value, keep flag) per input point in place of that range, a device
-// scan turns flags into output positions, and K5c scatters the kept points.  The keep
-// rule reproduces reduce_pair's emission: a point at every distinct breakpoint whose
-// combined value differs from the value of the cell just before it (equivalently, from
-// the last emitted value), the t = 0 point always.
+// The finalisation flags every point of the root node(s) -- keep where the scaled value
+// differs from the previous surviving point's (minimize_discretization), drop zero-width
+// pieces left by non-compacting levels -- and pcf_compact turns the flags into positions
+// (device exclusive scan) and scatters the kept points and the node offsets.
 #define CCCL_IGNORE_DEPRECATED_API 1
 #include <cub/cub.cuh>
 #include "pcf_common.cuh"
@@ -22,7 +16,7 @@ template <typename T> __device__ __forceinline__ T to_t(double x);
 template <> __device__ __forceinline__ double to_t<double>(double x) { return x; }
 template <> __device__ __forceinline__ float to_t<float>(double x) { return __double2float_rn(x); }
 
-// ------------------------------------------------------------ compaction (K5c)
+// ------------------------------------------------------------ compaction
 template <typename T, typename V>
 __global__ void k_scatter(const T* __restrict__ st, const V* __restrict__ sv,
                           const V* __restrict__ sv2, const int32_t* __restrict__ flag,

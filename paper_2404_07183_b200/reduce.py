@@ -209,10 +209,14 @@ def _device_plan(seg_nodes, leaves0, moments, dev):
 
 
 def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=None):
-    """Reduce each fibre (seg_nodes[i] consecutive nodes) to one node: one tiled
-    two-pass level kernel per tree level (pcf_tree_level).  The whole pairing plan is
-    uploaded once and the levels run back to back with no host synchronisation (each
-    level's point count is read on the device; the host passes an upper bound)."""
+    """Reduce each fibre (seg_nodes[i] consecutive nodes) to one node: one tiled level
+    kernel per tree level -- compacting (pcf_tree_level) for level 0, and for the upper
+    levels too unless level 0 kept >= 90% of its candidates, in which case they run as
+    non-compacting merges (pcf_tree_merge_level; zero-width pieces are dropped by
+    _finalize).  The pairing plan is uploaded once (cached per tree shape) and the levels
+    run back to back; the only host synchronisation is the level-0 kept count in auto
+    mode (each level's point count is read on the device; the host passes an upper bound).
+    The returned level lives in cached scratch: consume or copy it before the next tree."""
     torch = _torch()
     lib = _native.load()
     dev = level.t.device
