@@ -878,7 +878,11 @@ int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
     return PCF_ERR_ARG;
   }
   if (ntot <= 0) {
-    cudaMemsetAsync(off_out_dev, 0, (nout + 1) * sizeof(int64_t), s);
+    const cudaError_t e0 = cudaMemsetAsync(off_out_dev, 0, (nout + 1) * sizeof(int64_t), s);
+    if (e0 != cudaSuccess) {
+      set_error("pcf_tree_level: %s", cudaGetErrorString(e0));
+      return PCF_ERR_CUDA;
+    }
     return PCF_OK;
   }
   const int64_t ntiles = (ntot + LT - 1) / LT;
@@ -899,7 +903,13 @@ int pcf_tree_level(int kind, int is_f32, const void* t_dev, const void* v_dev,
   void* x_t = xbase;
   void* x_v = xbase + 8 * ntot;
   double* x_v2 = (double*)(xbase + 16 * ntot);
-  cudaMemsetAsync(tile_status, 0, (ntiles + 1) * 8 + 16, s);
+  {
+    const cudaError_t e0 = cudaMemsetAsync(tile_status, 0, (ntiles + 1) * 8 + 16, s);
+    if (e0 != cudaSuccess) {
+      set_error("pcf_tree_level: %s", cudaGetErrorString(e0));
+      return PCF_ERR_CUDA;
+    }
+  }
   const int pg = (int)((ntiles + 1 + 255) / 256);
   const unsigned grid = (unsigned)ntiles;
 #define PCF_TL(T, K)                                                                          \
