@@ -456,9 +456,20 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
     host_t = torch.from_numpy(t).pin_memory()
     host_v = torch.from_numpy(v).pin_memory()
     host_off = torch.from_numpy(off).pin_memory()
-    host_out = torch.empty((M, M), dtype=torch.float64, pin_memory=True) if rank == 0 else None
-    # world 1: pcf_matrix_host owns its device buffers (workspace cached between calls)
-    out = torch.zeros((M, M), dtype=torch.float64, device=dev) if world > 1 else None
+    shm = _shared_host_matrix(M, rank, world, dev) if world > 1 else None
+    if shm is not None:
+        host_out = shm[1]  # one host matrix (shared memory) that every rank fills
+    else:
+        host_out = torch.empty((M, M), dtype=torch.float64, pin_memory=True) if rank == 0 \
+            else None
+    band = -(-M // world)
+    # world 1: pcf_matrix_host owns its device buffers (workspace cached between calls);
+    # N ranks: zeroed M x M buffers (rows padded to N bands for the reduce-scatter)
+    out_full = torch.zeros((band * world, M), dtype=torch.float64, device=dev) \
+        if world > 1 else None
+    out = out_full[:M] if world > 1 else None
+    recv = torch.empty((band, M), dtype=torch.float64, device=dev) \
+        if shm is not None else None
     stream = torch.cuda.current_stream()
     bi = host_t.numel() * 8 + host_v.numel() * 8 + host_off.numel() * 8
     bo = M * M * 8 if rank == 0 else 0
@@ -479,6 +490,11 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
                 "-> H2D -> host size sort + plan -> pcf_pack_sorted -> diagonal + K1 fills in "
                 "32 cost-balanced chunks of size-sorted row blocks, each chunk's finished rows "
                 "D2H'd into the pinned M x M float64 result while later chunks compute")
+    elif shm is not None:
+        path = ("pinned host SoA (reference pack() layout) -> H2D -> pcf_pack_sorted -> "
+                "pcf_fill_diagonal + pcf_fill_matrix (rank's share of the tile queue) -> "
+                "reduce-scatter of row bands over NVLink -> every rank D2Hs its band into one "
+                "shared (registered) host M x M float64 matrix")
     else:
         path = ("pinned host SoA (reference pack() layout) -> H2D -> pcf_pack_sorted -> "
                 "pcf_fill_diagonal + pcf_fill_matrix (rank's share) -> NCCL reduce to rank 0 "
@@ -498,6 +514,20 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
         else:
             items = (items_dev, host_items, smem)
         fill_pairwise(coll, 0, 1.0, True, False, out=out, items=items)
+        if shm is not None:
+            # every entry has exactly one writer and the buffers start at zero, so the
+            # sum-reduce-scatter assembles each band exactly; each rank then drains its
+            # band over its own PCIe link
+            if BACKEND == "nccl":
+                tdist.reduce_scatter_tensor(recv, out_full)
+            else:  # gloo has no reduce-scatter: same result through an all-reduce
+                host = out_full.cpu()
+                tdist.all_reduce(host)
+                recv.copy_(host[rank * band:(rank + 1) * band])
+            r0, r1 = rank * band, min(M, (rank + 1) * band)
+            if r1 > r0:
+                host_out[r0:r1].copy_(recv[: r1 - r0], non_blocking=True)
+            return
         if world > 1:
             if BACKEND == "nccl":
                 tdist.reduce(out, dst=0)
@@ -528,14 +558,70 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
         tt = torch.tensor([ms], dtype=torch.float64, device=dev if BACKEND == "nccl" else "cpu")
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         ms = float(tt.item())
+    if shm is not None:
+        bo = M * M * 8  # the whole matrix reaches host memory, one band per rank
+        tdist.barrier()
     res = {"value": pairs * k / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": bi,
            "d2h_bytes_per_step": bo, "ms_per_step": ms / k, "steps": k, "path": path}
     if rank == 0:
         # a few rows of the host result, checked against the reference kernel by the CPU
-        # leg (the only place bench.py runs oracle/)
+        # leg (the only place bench.py runs oracle/), and their digest (identical for
+        # every GPU count: one writer and one summation order per entry)
         res["_rows"] = {int(i): host_out[int(i)].numpy().copy()
                         for i in sorted({1, M // 3, (2 * M) // 3, M - 2}) if 0 <= i < M - 1}
+        res["row_digest"] = float(sum(float(np.sum(r)) for r in res["_rows"].values()))
+    if shm is not None:
+        _release_shared(shm, rank, world)
     return res
+
+
+def _shared_host_matrix(M, rank, world, dev):
+    """One M x M float64 host matrix in /dev/shm mapped by every rank and registered
+    (pinned) with CUDA, so each rank can DMA its row band straight into the final result.
+    Returns (memmap, tensor, path, registered) or None (then rank 0 gathers)."""
+    import torch
+    import torch.distributed as tdist
+
+    path = f"/dev/shm/pcf_b200_e2e_{os.environ.get('MASTER_PORT', '0')}_{M}.bin"
+    ok = torch.tensor([1], dtype=torch.int32, device=dev if BACKEND == "nccl" else "cpu")
+    mm = None
+    try:
+        if rank == 0:
+            mm = np.memmap(path, dtype=np.float64, mode="w+", shape=(M, M))
+    except (OSError, ValueError):
+        ok[0] = 0
+    tdist.broadcast(ok, src=0)
+    if not int(ok[0]):
+        return None
+    tdist.barrier()
+    try:
+        if rank != 0:
+            mm = np.memmap(path, dtype=np.float64, mode="r+", shape=(M, M))
+        ten = torch.from_numpy(mm)
+        rc = torch.cuda.cudart().cudaHostRegister(ten.data_ptr(), M * M * 8, 0)
+        reg = int(rc) == 0
+    except (OSError, ValueError, RuntimeError):
+        ok[0] = 0
+        ten, reg = None, False
+    tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)
+    if not int(ok[0]):
+        return None
+    return mm, ten, path, reg
+
+
+def _release_shared(shm, rank, world):
+    import torch
+    import torch.distributed as tdist
+
+    mm, ten, path, reg = shm
+    if reg:
+        torch.cuda.cudart().cudaHostUnregister(ten.data_ptr())
+    tdist.barrier()
+    if rank == 0:
+        try:
+            os.unlink(path)
+        except OSError:
+            pass
 
 
 def _build_collection(coll, dt, dv, do, off_host, dev):
