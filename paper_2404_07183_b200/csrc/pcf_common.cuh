@@ -110,6 +110,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Bulk prefetch of a global byte range into L2 (no completion tracking): warms the next
+// column chunk while the current one is walked, so its later bulk copy hits L2.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Largest count of x in [0, n) with key(x) <= a, for sorted keys (upper_bound).
 template <typename KeyF>
 __device__ __forceinline__ int upper_bound_count(int n, double a, KeyF key) {

@@ -262,6 +262,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const bool ok = row_ok && qs < ce && qs > ps;
       mbar_wait(&bars[1 + kb], ph_col[kb]);
       ph_col[kb] ^= 1u;
+      if (single && tid == 0 && c + 1 < nchunk) {
+        // single buffer: the next chunk's copy can only start after this walk; warm L2
+        const int nb0 = W.col0 + ((c + 1) << logC), ne = min(nb0 + C, W.col1);
+        const int64_t r0 = cstart(nb0);
+        bulk_prefetch_l2(recs + r0, (uint32_t)((cend(ne) - r0) * sizeof(RT)));
+      }
       const RT* Gv = reinterpret_cast<const RT*>(colbase + kb * col_al);
       double acc = 0.0, hl = 0.0;
       if (ok) {
