@@ -393,6 +393,10 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const bool ok = k < gk1 && qs >= W.col0 && qs < W.col1 && qs > ps && qs < M;
       mbar_wait(&bars[1 + kb], ph_col[kb]);
       ph_col[kb] ^= 1u;
+      if (single && tid == 0 && c + 1 < nchunk) {  // warm L2 for the next chunk's copy
+        const int nk0 = gk0 + ((c + 1) << logCG), nk1 = min(nk0 + CG, gk1);
+        bulk_prefetch_l2(recsg + goff[nk0], (uint32_t)((goff[nk1] - goff[nk0]) * sizeof(RT)));
+      }
       double acc = 0.0, hl = 0.0;
       if (ok) {
         const RT* Gv = reinterpret_cast<const RT*>(colbase + kb * col_al) +
