@@ -406,3 +406,40 @@ def test_matrix_host_equals_device_fill(case, oracle):
         if exact:
             assert np.array_equal(H[5, 6:], ref[6:])
         assert rel_err(H[5, 6:], ref[6:]) < TOL64
+
+
+@pytest.mark.parametrize("f32", [False, True])
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("bounds", [(0.0, math.inf), (0.2, 0.85)])
+def test_all_tile_kernels_against_oracle(oracle, f32, exact, bounds):
+    """A heavy-tailed collection whose plan uses every tile kernel (K1, K1c for long rows
+    against short column groups, K1r for long x long pairs, K1g in exact mode) at the
+    default shared-memory budget; rows against the C oracle (p = 1 bitwise in exact mode)."""
+    from paper_2404_07183_b200.collection import DeviceCollection
+    from paper_2404_07183_b200.engine import decode_err, fill_pairwise
+
+    t, v, off = dg.pack_matrices(dg.ecc_like_collection(300, nmax_exp=3.7))
+    if f32:
+        t, v = t.astype(np.float32), v.astype(np.float32)
+    coll = DeviceCollection(t, v, off)
+    _, host, _ = coll.plan(exact=exact)
+    modes = set(host[:, 6].tolist())
+    assert {1, 2, 3} <= modes, modes
+    a, b = bounds
+    tt, vv = t.astype(np.float64), v.astype(np.float64)
+    rows = [0, 3, 40, 150, 298]
+    for p in (1.0, 2.0):
+        out, err, _ = fill_pairwise(coll, 0, p, True, False, a=a, b=b, exact=exact)
+        assert decode_err(err, coll.M) is None
+        D = out.cpu().numpy().astype(np.float64)
+        assert np.array_equal(D, D.T)
+        for i in rows:
+            ref = oracle.row(tt, vv, off, i, p=p, a=a, b=b)
+            got, want = D[i, i + 1:], ref[i + 1:]
+            if f32:
+                want = want.astype(np.float32).astype(np.float64)
+                assert rel_err(got, want) < TOL32
+            elif exact and p == 1.0:
+                assert np.array_equal(got, want), i
+            else:
+                assert rel_err(got, want) < TOL64, i
