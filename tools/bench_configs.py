@@ -43,7 +43,9 @@ def dev_time(fn, reps=3):
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
+    out = None
     for _ in range(reps):
+        out = None  # the previous result is released before the next call allocates
         out = fn()
     b.record()
     torch.cuda.synchronize()
@@ -98,8 +100,12 @@ def matrix_case(name, t, v, off, op, p, root, diag, exact_ok, tol, sample_rows):
     pairs = M * (M + 1) // 2 if diag else M * (M - 1) // 2
     coll = DeviceCollection(t, v, off)
     res = {"config": name, "M": M, "pairs": pairs}
+    # one output buffer for every timed call: a fresh M x M allocation inside the timed
+    # region would time the allocator, not the kernels
+    buf = torch.empty((M, M), dtype=coll.out_torch_dtype, device=coll.device)
     for exact in ([False, True] if exact_ok else [False]):
-        ms, (out, err, _) = dev_time(lambda: fill_pairwise(coll, op, p, root, diag, exact=exact))
+        ms, (out, err, _) = dev_time(lambda: fill_pairwise(coll, op, p, root, diag, out=buf,
+                                                           exact=exact))
         D = out.cpu().numpy()
         key = "exact" if exact else "fast"
         res[key] = {"ms": ms, "pairs_per_s": pairs / ms * 1e3, "err": decode_err(err, M)}
