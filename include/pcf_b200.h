@@ -160,7 +160,7 @@ int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* o
                         double a, double b, double* out, int64_t ld, int64_t* err_i,
                         int64_t* err_j);
 
-/* Whole matrix from host buffers: MatrixJob.run over the compiled module
+/* Whole matrix from host buffers (serialised per process): MatrixJob.run over the compiled module
  * (pkg/src/pcflib/matrix.py:156-234 -> pack, fill_block per row block; pyx:72-121) in one
  * call.  tcat/vcat/off: the reference pack() layout in host memory (float64, or float32
  * when is_f32); out: host M x M (leading dimension ld) of the same kind, written in

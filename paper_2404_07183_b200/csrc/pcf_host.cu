@@ -24,6 +24,7 @@
 #include <string.h>
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <numeric>
 #include <vector>
 #include "pcf_internal.h"
@@ -71,6 +72,7 @@ struct Workspace {
   }
 };
 Workspace g_ws;
+std::mutex g_ws_mutex;  // one whole-matrix call at a time per process (shared workspace)
 
 // ld.global-style row copy list for one chunk: original row perm[s] of the device matrix
 // to the same row of the host matrix
@@ -126,7 +128,10 @@ using namespace pcfb;
 
 extern "C" {
 
-void pcf_release_workspace(void) { g_ws.release(); }
+void pcf_release_workspace(void) {
+  std::lock_guard<std::mutex> lock(g_ws_mutex);
+  g_ws.release();
+}
 
 int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_t* off, int64_t M,
                     int op, double p, int apply_root, int diag, double a, double b,
@@ -140,6 +145,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
     return PCF_ERR_ARG;
   }
   if (n_chunks < 1) n_chunks = 1;
+  std::lock_guard<std::mutex> lock(g_ws_mutex);
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(e, "pcf_matrix_host device");
