@@ -22,6 +22,7 @@ from __future__ import annotations
 import math
 import operator
 import os
+import threading
 
 import numpy as np
 
@@ -155,14 +156,21 @@ def _plan_levels(seg_nodes, leaves0=None, moments=False):
 
 
 _PLAN_CACHE = {}
-_SCRATCH = {}
+_SCRATCH_TLS = threading.local()  # per thread: a tree's output lives here until consumed
+
+
+def _scratch_dict():
+    d = getattr(_SCRATCH_TLS, "bufs", None)
+    if d is None:
+        d = _SCRATCH_TLS.bufs = {}
+    return d
 
 
 def _in_scratch(x):
     if x is None:
         return False
     p = x.data_ptr()
-    for buf in _SCRATCH.values():
+    for buf in _scratch_dict().values():
         b = buf.data_ptr()
         if b <= p < b + buf.numel() * buf.element_size():
             return True
@@ -175,11 +183,12 @@ def _scratch(name, numel, dtype, dev):
     output level is copied out by _finalize / to_pcfs before the next tree runs."""
     torch = _torch()
     key = (name, dtype, str(dev))
-    buf = _SCRATCH.get(key)
+    cache = _scratch_dict()
+    buf = cache.get(key)
     if buf is None or buf.numel() < numel:
-        _SCRATCH.pop(key, None)
+        cache.pop(key, None)
         buf = torch.empty(max(int(numel), 1), dtype=dtype, device=dev)
-        _SCRATCH[key] = buf
+        cache[key] = buf
     return buf[:numel]
 
 
