@@ -201,6 +201,21 @@ int pcf_jit_matrix(void* module, const void* recs_dev, const int64_t* soff_dev,
 int pcf_jit_pairs(void* module, const void* recs_dev, const int64_t* soff_dev,
                   const int64_t* pairs_dev, int64_t npairs, double a, double b, int out_f32,
                   double* res_dev, int32_t* status_dev, void* stream);
+/* The tile kernels K1 / K1c / K1r / K1g (pcf_fill_matrix) instantiated for a user
+ * integrand h (PCF_MODE 0, declared symmetric): NVRTC compiles csrc/pcf_tiles.cuh with
+ * h in place of |x - y|^p and r in place of the p-th root, for one record kind
+ * (is_f32: 8-byte float32 records, float output).  Replaces the per-rectangle Python
+ * callback of the reference's custom-integral matrix (pkg/src/pcflib/matrix.py:184-196).
+ * Fills the strict upper triangle of the plan's pairs, mirrored (the diagonal is the
+ * caller's: pcf_jit_pairs on (s, s)); err_dev (init UINT64_MAX): atomicMin of the
+ * (min, max) original-index key of the first non-finite / divergent entry. */
+int pcf_jit_tiles_load(const char* defs, int is_f32, void** module, char* log, int64_t logcap);
+void pcf_jit_tiles_release(void* module);
+int pcf_jit_fill_tiles(void* module, int smem_mode, const void* recs_dev, const void* recsg_dev,
+                       const int64_t* soff_dev, const int64_t* goff_dev, const int32_t* perm_dev,
+                       int64_t M, const void* items_dev, int64_t n_items, int32_t smem_bytes,
+                       int32_t* counter_dev, int has_r, double a, double b, void* out_dev,
+                       int64_t ld, unsigned long long* err_dev, void* stream);
 /* integrate_single of every (sorted) PCF with pcf_u */
 int pcf_jit_single(void* module, const void* recs_dev, const int64_t* soff_dev, int64_t M,
                    double a, double b, int out_f32, double* res_dev, int32_t* status_dev,

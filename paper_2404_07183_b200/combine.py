@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -178,13 +179,137 @@ def integrate_single(f, h, a=0.0, b=_INF) -> float:
     return float(integrate_single_many([f], h, a, b)[0])
 
 
-def fill_custom(coll, integral: CombinationIntegral, out, row_chunks=1, between=None):
+_PROBE = (0.0, 1.0, -1.0, 0.5, 2.5, -2.25, 1e-3, 3.75, 7.0, 1e10, -1e-7, 0.1)
+
+
+def _probably_symmetric(h):
+    """Does h(x, y) == h(y, x) bitwise on a fixed probe set (Python evaluation)?  Only
+    then may the tile kernels, which walk a pair in either orientation, run a
+    `symmetric=True` integral; otherwise the one-thread path keeps the reference's
+    orientation (f = the lower original index, matrix.py:186-193)."""
+    try:
+        for x in _PROBE:
+            for y in _PROBE:
+                u, w = float(h(x, y)), float(h(y, x))
+                if not (u == w or (u != u and w != w)):
+                    return False
+                if u == w and u == 0.0 and math.copysign(1.0, u) != math.copysign(1.0, w):
+                    return False
+    except Exception:
+        return False
+    return True
+
+
+def _tiles_eligible(integral):
+    return (integral.h is not None and integral.symmetric
+            and os.environ.get("PCF_JIT_NO_TILES", "") in ("", "0")
+            and _probably_symmetric(integral.h))
+
+
+def _fill_custom_tiles(coll, integral, out, exact, chunks, between):
+    """Symmetric pointwise integrands on the tile kernels (K1 / K1c / K1r / K1g compiled
+    with h, pcf_jit_fill_tiles): strict upper triangle from the collection's work plan
+    (exact: one lane per pair, the reference's left-to-right sum), diagonal by
+    pcf_jit_pairs on (s, s).  Same return as fill_custom."""
+    from .collection import current_stream_handle
+    from .engine import mode_runs
+
+    torch = _torch()
+    lib = _native.load()
+    a, b = _bounds(integral.a, integral.b)
+    defs = jit.generate(h=integral.h, r=integral.r)
+    mod = jit.JitModule.get(defs)
+    tiles = jit.JitTiles.get(defs, coll.dtype == np.float32)
+    M = coll.M
+    out_f32 = int(out.dtype == torch.float32)
+    st = current_stream_handle()
+    items_dev, host_items, smem = coll.plan(exact=exact)
+    err = torch.full((1,), -1, dtype=torch.int64, device=coll.device)
+    counter = torch.zeros(1, dtype=torch.int32, device=coll.device)
+    # diagonal: <f, f> entries through the one-thread kernel
+    idx = torch.arange(M, dtype=torch.int64, device=coll.device)
+    pd = torch.stack((idx, idx), 1).reshape(-1).contiguous()
+    dres = torch.empty(M, dtype=torch.float64, device=coll.device)
+    dst = torch.empty(M, dtype=torch.int32, device=coll.device)
+    _native.check(lib.pcf_jit_pairs(
+        mod.handle, _native.ptr(coll.recs), _native.ptr(coll.soff), _native.ptr(pd), M, a, b,
+        out_f32, _native.ptr(dres), _native.ptr(dst), st), "pcf_jit_pairs")
+    perm = coll.perm.long()
+    out[perm, perm] = dres.to(out.dtype)
+    segs = []
+    for base, end, mode in mode_runs(host_items):
+        count = end - base
+        k = max(1, min(int(chunks), count))
+        bnd = [base + (count * i) // k for i in range(k + 1)]
+        segs += [(bnd[i], bnd[i + 1], mode) for i in range(k) if bnd[i + 1] > bnd[i]]
+    events = []
+    for n, (s0, s1, mode) in enumerate(segs):
+        _native.check(lib.pcf_jit_fill_tiles(
+            tiles.handle, mode, _native.ptr(coll.tile_recs), _native.ptr(coll.recsg),
+            _native.ptr(coll.soff), _native.ptr(coll.goff), _native.ptr(coll.perm), M,
+            _native.c_vp(items_dev.data_ptr() + s0 * 32), s1 - s0, smem, _native.ptr(counter),
+            int(tiles.has_r), a, b, _native.ptr(out), out.stride(0), _native.ptr(err), st),
+            "pcf_jit_fill_tiles")
+        if between is not None:
+            ev = torch.cuda.Event()
+            ev.record()
+            events.append(ev)
+            if len(events) >= 2:
+                events[-2].synchronize()
+                if between(n / len(segs)):
+                    return None, True
+    if between is not None:
+        if events:
+            events[-1].synchronize()
+        between(1.0)
+    # first failing entry in row-major (min, max) order: the tile kernels report the
+    # key only; its status comes from the one-thread kernel on the same pair
+    cand = []
+    bad = torch.nonzero(dst).reshape(-1)
+    if bad.numel():
+        o = perm[bad]
+        k = int(torch.min(o).item())
+        cand.append((k * M + k, k, k))
+    key = int(err.item()) & 0xFFFFFFFFFFFFFFFF
+    if key != 2 ** 64 - 1:
+        cand.append((key, key // M, key % M))
+    if not cand:
+        return None, False
+    _, i, j = min(cand)
+    if i == j:
+        stt = int(dst[int(coll.inv[i].item())].item())
+    else:
+        inv = coll_inv(coll)
+        pair = torch.tensor([inv[i], inv[j]], dtype=torch.int64, device=coll.device)
+        r1 = torch.empty(1, dtype=torch.float64, device=coll.device)
+        s1_ = torch.empty(1, dtype=torch.int32, device=coll.device)
+        _native.check(lib.pcf_jit_pairs(
+            mod.handle, _native.ptr(coll.recs), _native.ptr(coll.soff), _native.ptr(pair), 1,
+            a, b, out_f32, _native.ptr(r1), _native.ptr(s1_), st), "pcf_jit_pairs")
+        stt = int(s1_.item()) or 2
+    return (stt, i, j), False
+
+
+def coll_inv(coll):
+    inv = np.empty(coll.M, dtype=np.int64)
+    inv[coll.perm_host] = np.arange(coll.M)
+    return inv
+
+
+def fill_custom(coll, integral: CombinationIntegral, out, row_chunks=1, between=None,
+                exact=True):
     """Custom-integral matrix (MatrixJob with integral=, matrix.py:184-196) into the
     device tensor `out` (original order).  Symmetric integrals: q >= s, mirrored
     (diagonal included); otherwise all M^2 entries.  Returns (err, stopped) where err is
-    None or (status, i, j) of the first failing entry in row-major order."""
+    None or (status, i, j) of the first failing entry in row-major order.
+
+    Symmetric pointwise integrands run on the tile kernels (exact: one lane per pair,
+    the reference's cell order; exact=False lets a warp share a long pair); the others,
+    time-dependent ones, and h that fail the symmetry probe run one thread per entry."""
     from .collection import current_stream_handle
 
+    if _tiles_eligible(integral):
+        return _fill_custom_tiles(coll, integral, out, exact, row_chunks, between)
     torch = _torch()
     lib = _native.load()
     a, b = _bounds(integral.a, integral.b)

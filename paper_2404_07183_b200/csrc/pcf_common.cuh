@@ -8,9 +8,19 @@
 // size-sorted (descending) and concatenated, so any run of consecutive PCFs is one
 // contiguous byte range -> one cp.async.bulk copy.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#else  // NVRTC (user integrands, pcf_jit.cu): no host headers
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+#ifndef INFINITY
+#define INFINITY __int_as_float(0x7f800000)
+#endif
+#endif
 
 namespace pcfb {
 
@@ -28,7 +38,12 @@ struct __align__(8) Rec32 {
 
 // Integrand kinds.  OP_LP with p=1/2/3 get exact-arithmetic specialisations; any
 // other p goes through pow().  OP_INNER is v_f * v_g.
-enum HKind { H_L1 = 0, H_L2 = 1, H_L3 = 2, H_LP = 3, H_INNER = 4 };
+enum HKind { H_L1 = 0, H_L2 = 1, H_L3 = 2, H_LP = 3, H_INNER = 4, H_USER = 5 };
+
+// A user integrand compiled at run time (pcf_jit.cu defines it; never referenced by the
+// nvcc-built kernels, where HK is one of the op codes above).
+__device__ double pcf_user_h(double x, double y);
+__device__ double pcf_user_r(double x);
 
 // h(v_f, v_g): _sweepkern.pyx:43-46.  Rounded ops only (no FMA contraction) so the
 // p=1 and inner-product paths reproduce the gcc -O2 (SSE2, no FMA) reference bitwise.
@@ -44,6 +59,7 @@ __device__ __forceinline__ double hval(double x, double y, double p) {
     return __dmul_rn(__dmul_rn(d, d), d);
   }
   if (HK == H_LP) return pow(fabs(__dsub_rn(x, y)), p);
+  if constexpr (HK == H_USER) return pcf_user_h(x, y);
   return __dmul_rn(x, y);
 }
 

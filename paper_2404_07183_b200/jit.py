@@ -470,6 +470,41 @@ class JitModule:
             return mod
 
 
+class JitTiles:
+    """The tile kernels compiled for one generated integrand and record kind (cached);
+    csrc/pcf_jit.cu pcf_jit_tiles_load."""
+
+    _cache = {}
+    _lock = threading.Lock()
+
+    def __init__(self, handle, defs, f32):
+        self.handle = handle
+        self.defs = defs
+        self.f32 = f32
+        self.has_r = "#define PCF_HAS_R 1" in defs
+
+    @classmethod
+    def get(cls, defs, f32):
+        key = (hashlib.sha1(defs.encode()).hexdigest(), bool(f32))
+        with cls._lock:
+            mod = cls._cache.get(key)
+            if mod is None:
+                lib = _native.load()
+                h = ctypes.c_void_p()
+                log = ctypes.create_string_buffer(8192)
+                rc = lib.pcf_jit_tiles_load(defs.encode(), int(bool(f32)), ctypes.byref(h), log,
+                                            8192)
+                if rc != 0:
+                    msg = lib.pcf_last_error().decode(errors="replace")
+                    if rc == 1:
+                        raise errors.UnsupportedIntegrand(
+                            f"device compilation failed: {log.value.decode(errors='replace')}")
+                    raise errors.BackendUnavailable(msg)
+                mod = cls(h, defs, bool(f32))
+                cls._cache[key] = mod
+            return mod
+
+
 def compile_only(defs):
     """NVRTC-compile without a GPU (CUBIN size); raises UnsupportedIntegrand on errors."""
     lib = _native.load()

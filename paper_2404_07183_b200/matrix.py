@@ -132,6 +132,7 @@ class MatrixJob:
         to right like the reference (bitwise for p=1 and the Gram matrix); the default
         (env PCF_B200_EXACT unset) lets up to a warp share a long pair, which sums the
         same cell products in a different order (relative error < 1e-13 for L_p)."""
+        exact_arg = exact
         if exact is None:
             exact = os.environ.get("PCF_B200_EXACT", "") not in ("", "0")
         resolve_workers(workers)
@@ -151,7 +152,7 @@ class MatrixJob:
             return self._cancel.is_set()
 
         if self._integral is not None:
-            return self._run_custom(coll, report, device_output)
+            return self._run_custom(coll, report, device_output, exact_arg)
         out, err, stopped = fill_pairwise(
             coll, self._op, self._p, self._apply_root, self._diag, self._a, self._b,
             chunks=_PROGRESS_SLICES if self._sinks else 1,
@@ -165,10 +166,11 @@ class MatrixJob:
         data = out if device_output else out.cpu().numpy()
         return PairwiseMatrix(data, True, self.entries_computed)
 
-    def _run_custom(self, coll, report, device_output):
+    def _run_custom(self, coll, report, device_output, exact=None):
         """Arbitrary CombinationIntegral (matrix.py:184-196): the integrand is compiled
         for the device (jit.py); symmetric integrals fill one triangle incl. the
-        diagonal and mirror it, asymmetric ones all M^2 entries."""
+        diagonal and mirror it, asymmetric ones all M^2 entries.  Custom integrals are
+        exact (the reference's per-entry sum order) unless exact=False is passed."""
         import torch
 
         from .combine import _status_error, fill_custom
@@ -177,7 +179,8 @@ class MatrixJob:
         out = torch.zeros((M, M), dtype=coll.out_torch_dtype, device=coll.device)
         err, stopped = fill_custom(coll, self._integral, out,
                                    row_chunks=_PROGRESS_SLICES if self._sinks else 1,
-                                   between=report if self._sinks else None)
+                                   between=report if self._sinks else None,
+                                   exact=exact is not False)
         if stopped or self._cancel.is_set():
             raise errors.Cancelled("matrix job cancelled; partial work discarded")
         if err is not None:
@@ -226,10 +229,13 @@ def pairwise_job(collection, integral) -> MatrixJob:
     return MatrixJob(collection, integral=integral)
 
 
-def pairwise(collection, integral, workers=None, device_output=False) -> PairwiseMatrix:
+def pairwise(collection, integral, workers=None, device_output=False,
+             exact=None) -> PairwiseMatrix:
     """Pairwise integrated combination matrix under an arbitrary CombinationIntegral
-    (matrix.py:279-283); the integrand runs on the device (jit.py)."""
-    return pairwise_job(collection, integral).run(workers, device_output=device_output)
+    (matrix.py:279-283); the integrand runs on the device (jit.py).  exact=False lets
+    the tile kernels split long pairs over a warp (symmetric h only)."""
+    return pairwise_job(collection, integral).run(workers, device_output=device_output,
+                                                  exact=exact)
 
 
 def progress_subscribe(job: MatrixJob, sink) -> None:

@@ -23,8 +23,22 @@ cells = (M - 1) * int(n.sum()) - M * (M - 1) // 2
 coll = DeviceCollection(t, v, off)
 out = torch.empty((M, M), dtype=torch.float64, device="cuda")
 ci = CombinationIntegral(h=absdiff, symmetric=True)
+
+
+def one_thread():
+    os.environ["PCF_JIT_NO_TILES"] = "1"
+    try:
+        return fill_custom(coll, ci, out)
+    finally:
+        del os.environ["PCF_JIT_NO_TILES"]
+
+
 for name, fn in (("op-coded L1 (K1)", lambda: fill_pairwise(coll, 0, 1.0, False, False, out=out)),
-                 ("JIT h=abs(x-y)", lambda: fill_custom(coll, ci, out))):
+                 ("op-coded L1 exact", lambda: fill_pairwise(coll, 0, 1.0, False, False, out=out,
+                                                             exact=True)),
+                 ("JIT tiles", lambda: fill_custom(coll, ci, out, exact=False)),
+                 ("JIT tiles exact", lambda: fill_custom(coll, ci, out, exact=True)),
+                 ("JIT one thread", one_thread)):
     fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
