@@ -95,7 +95,14 @@ __device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
   for (int s = 0; s < steps; ++s) {
     double tn = (double)tx;
     if (BOUNDED) tn = fmin(tn, b);
-    acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(tn, t)));
+    if constexpr (HK == H_USER) {
+      // a user h may be non-finite on the (v_X', v_Y) pair of a tie's zero-width cell or
+      // past b, which the reference never evaluates: skip those cells outright
+      const double dt = __dsub_rn(tn, t);
+      acc = __dadd_rn(acc, __dmul_rn(dt > 0.0 ? hc : 0.0, dt));
+    } else {
+      acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(tn, t)));
+    }
     t = tn;
     xp += xs;
     const ST nt = xp->t, nv = xp->v;
@@ -113,7 +120,7 @@ __device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
     ty = sw ? nt : ty;
     vy = sw ? nv : vy;
   }
-  if (BOUNDED && (lane == (1 << log2G) - 1)) {
+  if (BOUNDED && (lane == (1 << log2G) - 1) && (HK != H_USER || b > t)) {
     acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(b, t)));
   }
   return acc;

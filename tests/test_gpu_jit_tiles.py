@@ -139,3 +139,23 @@ def test_tile_path_errors(monkeypatch):
     with pytest.raises(errors.NonFinite) as info2:
         one_thread(monkeypatch, fs, nan_ci)
     assert info.value.pair == info2.value.pair
+
+
+def test_user_h_not_evaluated_on_tie_cells(monkeypatch):
+    """Simultaneous jumps: the tile walk takes them as two steps with a zero-width cell
+    between, whose value pair ((5, 2) or (1, 7) here) the reference never evaluates; a
+    user h that is infinite there must not leak into the sum."""
+    f = pb.make_pcf(np.array([[0.0, 1.0], [1.0, 5.0], [2.0, 0.0]]))
+    g = pb.make_pcf(np.array([[0.0, 2.0], [1.0, 7.0], [2.0, 0.0]]))
+
+    def h(x, y):
+        return 1.0 / ((x * y - 10.0) * (x * y - 7.0))
+
+    ci = pb.CombinationIntegral(h=h, a=0.0, b=3.0, symmetric=True)
+    ref = one_thread(monkeypatch, [f, g], ci)
+    assert np.isfinite(ref).all()
+    assert ref[0, 1] == (1.0 / 40.0 + 1.0 / 700.0) + 1.0 / 70.0
+    assert np.array_equal(np.asarray(pb.pairwise([f, g], ci)), ref)
+    assert np.array_equal(np.asarray(pb.pairwise([f, g], ci, exact=False)), ref)
+    ci2 = pb.CombinationIntegral(h=h, a=0.0, b=2.0, symmetric=True)  # b on a breakpoint
+    assert np.array_equal(np.asarray(pb.pairwise([f, g], ci2)), one_thread(monkeypatch, [f, g], ci2))
