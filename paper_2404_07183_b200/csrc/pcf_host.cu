@@ -5,16 +5,20 @@
 // One call takes the reference's pack() layout in host memory (tcat, vcat, off) and
 // returns the dense matrix in host memory, original order.  On the device:
 //
-//   H2D (SoA + size sort + plan) -> K3 pack -> diagonal -> K1/K1r/K1g fills in CHUNKS of
-//   consecutive size-sorted row blocks  ==>  D2H of each chunk's finished rows on a
-//   second stream while the next chunk computes.
+//   H2D (SoA + size sort + plan) -> K3 pack -> diagonal -> K1/K1c/K1r/K1g fills over a
+//   queue in column-sweep order, cut into cost-balanced CHUNKS  ==>  D2H of the rows each
+//   chunk finishes on two copy streams while later chunks compute.
 //
 // Row s of the size-sorted order is complete once every item whose row block contains s
 // (its pairs (s, q > s)) and every item whose columns contain s (row blocks before s) has
-// run; processing row blocks in ascending order therefore finishes rows in order, and the
-// D2H of chunk k (one contiguous M-entry row per finished PCF, scattered through perm to
-// its original row) overlaps the compute of chunks k+1, ...  The 80 GB result of the 100k
-// benchmark leaves the device while the kernels run instead of after them.
+// run.  The queue sweeps the column ranges right to left, so the short high rows finish
+// first and few rows remain at the end; the host computes, per chunk, the rows it
+// finishes (the last chunk touching each row), and the D2H of those rows (one contiguous
+// M-entry row per PCF, scattered through perm to its original row) overlaps the compute of
+// the later chunks.  The 80 GB result of the 100k benchmark leaves the device while the
+// kernel runs instead of after it.  With one kernel kind the whole queue is ONE
+// persistent launch whose items bump per-chunk completion counters
+// (cuStreamWaitValue32 on the copy streams).
 //
 // Device buffers come from a grow-only workspace kept between calls (like a caching
 // allocator); pcf_release_workspace() frees it.
@@ -74,17 +78,18 @@ struct Workspace {
 Workspace g_ws;
 std::mutex g_ws_mutex;  // one whole-matrix call at a time per process (shared workspace)
 
-// ld.global-style row copy list for one chunk: original row perm[s] of the device matrix
-// to the same row of the host matrix
-cudaError_t copy_rows(const std::vector<int32_t>& perm, int64_t s0, int64_t s1, const char* dsrc,
-                      char* hdst, int64_t M, int64_t ld, size_t es, cudaStream_t st) {
-  const size_t n = (size_t)(s1 - s0);
+// row copy list for one chunk: original row perm[s] of the device matrix to the same row
+// of the host matrix, for every sorted row s the chunk finishes
+cudaError_t copy_rows(const std::vector<int32_t>& perm, const std::vector<int32_t>& rows,
+                      const char* dsrc, char* hdst, int64_t M, int64_t ld, size_t es,
+                      cudaStream_t st) {
+  const size_t n = rows.size();
   static const bool no_d2h = getenv("PCF_HOST_NO_D2H") != nullptr;  // timing experiments
   if (n == 0 || no_d2h) return cudaSuccess;
   std::vector<void*> dst(n), src(n);
   std::vector<size_t> sizes(n, (size_t)M * es);
   for (size_t k = 0; k < n; ++k) {
-    const int64_t o = perm[s0 + (int64_t)k];
+    const int64_t o = perm[rows[k]];
     src[k] = (void*)(dsrc + (size_t)o * (size_t)M * es);
     dst[k] = (void*)(hdst + (size_t)o * (size_t)ld * es);
   }
@@ -179,6 +184,21 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
       return PCF_ERR_ARG;
     }
   }
+  // the raw time / value arrays go up first: their H2D overlaps the host planning below
+  const size_t es = is_f32 ? 4 : 8;
+  void *d_t, *d_v;
+  if ((e = g_ws.get(W_T, N * es, &d_t)) || (e = g_ws.get(W_V, N * es, &d_v)))
+    return fail(e, "pcf_matrix_host alloc");
+  // PCF_HOST_TIMING: device-side phase marks on s0 (upload start, fill start/end, done)
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (timing)
+    for (auto& ev : tev) cudaEventCreate(&ev);
+  if (timing) cudaEventRecord(tev[0], s0);
+  if ((e = cudaMemcpyAsync(d_t, (const char*)tcat + off[0] * es, N * es, cudaMemcpyHostToDevice,
+                           s0)) ||
+      (e = cudaMemcpyAsync(d_v, (const char*)vcat + off[0] * es, N * es, cudaMemcpyHostToDevice,
+                           s0)))
+    return fail(e, "pcf_matrix_host upload");
   std::vector<int32_t> perm(M);
   std::iota(perm.begin(), perm.end(), 0);
   std::stable_sort(perm.begin(), perm.end(),
@@ -191,59 +211,90 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   const int rec_bytes = is_f32 ? 8 : 16;
   const int GW = 128 / rec_bytes;
   std::vector<int64_t> goff((M + GW - 1) / GW + 1);
+  // (errors from here on first wait for the uploads already reading the caller's buffers)
   int rc = pcf_group_offsets(ss.data(), M, GW, goff.data());
-  if (rc) return rc;
+  if (rc) return cudaStreamSynchronize(s0), rc;
+  const double sort_ms = ms_since(t_start);
   int64_t n_items = 0;
   int32_t smem = 0;
   rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, 2048, max_log2G, rec_bytes, nullptr, 0,
                          &n_items, &smem);
-  if (rc) return rc;
+  if (rc) return cudaStreamSynchronize(s0), rc;
   std::vector<pcf_work_item> items(n_items > 0 ? n_items : 1);
   rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, 2048, max_log2G, rec_bytes, items.data(),
                          n_items, &n_items, &smem);
-  if (rc) return rc;
+  if (rc) return cudaStreamSynchronize(s0), rc;
   items.resize(n_items);
+  const double plan_ms = ms_since(t_start);
 
-  // ---- chunks of consecutive row blocks, cost-balanced, at most kRowsCap rows each
+  // ---- queue order: a right-to-left sweep over column ranges (col0 descending, then
+  // longest first).  Output row s is final once every item touching it has run -- its own
+  // row block's items and the items whose column range holds s -- and in sweep order the
+  // high (short, cheap) rows finish first and only the first few columns' rows finish at
+  // the end, so the D2H of the M x M result runs beside the fill instead of after it (row
+  // order would release half of the 80 GB in the last ~15% of the fill).
   auto item_cells = [&](const pcf_work_item& w) {
     const double rows_pts = (double)(soff[w.row0 + w.nrows] - soff[w.row0]);
     return (double)w.nrows * (double)(soff[w.col1] - soff[w.col0]) +
            (double)(w.col1 - w.col0) * rows_pts;
   };
-  std::stable_sort(items.begin(), items.end(), [](const pcf_work_item& x, const pcf_work_item& y) {
-    return x.row0 < y.row0;
+  static const bool row_order = getenv("PCF_HOST_ROW_ORDER") != nullptr;  // A/B timing
+  std::stable_sort(items.begin(), items.end(), [&](const pcf_work_item& x, const pcf_work_item& y) {
+    if (row_order) return x.row0 < y.row0;
+    if (x.col0 != y.col0) return x.col0 > y.col0;
+    return x.cost_hi > y.cost_hi;
   });
   double total = 0.0;
   for (auto& w : items) total += item_cells(w);
-  const int64_t kRowsCap = 2048;
-  struct Chunk { int64_t i0, i1, row_end; };
+  struct Chunk { int64_t i0, i1; };
   std::vector<Chunk> chunks;
   {
-    int64_t i = 0, start = 0, rows_start = 0;
+    const int64_t nc = std::max<int64_t>(n_chunks, 512);
+    int64_t start = 0;
     double acc = 0.0;
-    while (i < n_items) {
-      const int32_t r = items[i].row0;
-      int64_t j = i;
-      double c = 0.0;
-      int64_t rend = r;
-      while (j < n_items && items[j].row0 == r) {
-        c += item_cells(items[j]);
-        rend = std::max<int64_t>(rend, (int64_t)items[j].row0 + items[j].nrows);
-        ++j;
-      }
-      acc += c;
-      i = j;
-      if (acc >= total / n_chunks || rend - rows_start >= kRowsCap || i == n_items) {
-        chunks.push_back({start, i, i == n_items ? M : rend});
-        start = i;
-        rows_start = rend;
+    for (int64_t i = 0; i < n_items; ++i) {
+      acc += item_cells(items[i]);
+      if (acc >= total / nc || i + 1 == n_items) {
+        chunks.push_back({start, i + 1});
+        start = i + 1;
         acc = 0.0;
       }
     }
-    if (chunks.empty()) chunks.push_back({0, 0, M});
+    if (chunks.empty()) chunks.push_back({0, 0});
   }
-  // inside a chunk: one run per kernel (K1, K1r, K1g), each longest-first
-  auto mode_rank = [](int m) { return m == 1 ? 0 : (m == 2 ? 1 : 2); };
+  // rows finished by each chunk: done[s] = the last chunk touching s (assigned from the
+  // last chunk down, each row once, via a next-unassigned skip list)
+  std::vector<std::vector<int32_t>> chunk_rows(chunks.size());
+  {
+    std::vector<int32_t> owner(M, -1);
+    std::vector<int64_t> nxt(M + 1);
+    std::iota(nxt.begin(), nxt.end(), 0);
+    auto find = [&](int64_t x) {
+      int64_t r = x;
+      while (nxt[r] != r) r = nxt[r];
+      while (nxt[x] != r) {
+        const int64_t t = nxt[x];
+        nxt[x] = r;
+        x = t;
+      }
+      return r;
+    };
+    auto claim = [&](int64_t lo, int64_t hi, int32_t k) {
+      for (int64_t x = find(lo); x < hi; x = find(x)) {
+        owner[x] = k;
+        nxt[x] = x + 1;
+      }
+    };
+    for (int64_t k = (int64_t)chunks.size() - 1; k >= 0; --k)
+      for (int64_t i = chunks[k].i0; i < chunks[k].i1; ++i) {
+        const pcf_work_item& w = items[i];
+        claim(w.row0, std::min<int64_t>(w.row0 + w.nrows, M), (int32_t)k);
+        claim(std::max<int64_t>(w.col0, w.row0 + 1), w.col1, (int32_t)k);
+      }
+    for (int64_t x = 0; x < M; ++x) chunk_rows[owner[x] < 0 ? 0 : owner[x]].push_back((int32_t)x);
+  }
+  // inside a chunk: one run per kernel (K1, K1c, K1r, K1g), each longest-first
+  auto mode_rank = [](int m) { return m == 1 ? 0 : (m == 3 ? 1 : (m == 2 ? 2 : 3)); };
   for (auto& ch : chunks) {
     std::stable_sort(items.begin() + ch.i0, items.begin() + ch.i1,
                      [&](const pcf_work_item& x, const pcf_work_item& y) {
@@ -255,12 +306,10 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
 
   const double host_ms = ms_since(t_start);
   // ---- device buffers
-  const size_t es = is_f32 ? 4 : 8;
-  void *d_t, *d_v, *d_off, *d_perm, *d_soff, *d_goff, *d_recs, *d_recsg, *d_tile, *d_items,
+  void *d_off, *d_perm, *d_soff, *d_goff, *d_recs, *d_recsg, *d_tile, *d_items,
       *d_cnt, *d_err, *d_out;
   const int64_t ng = goff.back();
-  if ((e = g_ws.get(W_T, N * es, &d_t)) || (e = g_ws.get(W_V, N * es, &d_v)) ||
-      (e = g_ws.get(W_OFF, (M + 1) * 8, &d_off)) || (e = g_ws.get(W_PERM, M * 4, &d_perm)) ||
+  if ((e = g_ws.get(W_OFF, (M + 1) * 8, &d_off)) || (e = g_ws.get(W_PERM, M * 4, &d_perm)) ||
       (e = g_ws.get(W_SOFF, (M + 1) * 8, &d_soff)) ||
       (e = g_ws.get(W_GOFF, goff.size() * 8, &d_goff)) ||
       (e = g_ws.get(W_RECS, N * 16, &d_recs)) ||
@@ -269,7 +318,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
       (e = g_ws.get(W_ITEMS, std::max<int64_t>(n_items, 1) * sizeof(pcf_work_item), &d_items)) ||
       (e = g_ws.get(W_CNT, 64, &d_cnt)) || (e = g_ws.get(W_ERR, 8, &d_err)) ||
       (e = g_ws.get(W_OUT, (size_t)M * (size_t)M * es, &d_out)))
-    return fail(e, "pcf_matrix_host alloc");
+    return cudaStreamSynchronize(s0), fail(e, "pcf_matrix_host alloc");
 
   // rebase offsets to 0 if the caller passed a slice
   std::vector<int64_t> off0;
@@ -279,11 +328,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
     for (int64_t i = 0; i <= M; ++i) off0[i] = off[i] - off[0];
     offp = off0.data();
   }
-  const char* tsrc = (const char*)tcat + off[0] * es;
-  const char* vsrc = (const char*)vcat + off[0] * es;
-  if ((e = cudaMemcpyAsync(d_t, tsrc, N * es, cudaMemcpyHostToDevice, s0)) ||
-      (e = cudaMemcpyAsync(d_v, vsrc, N * es, cudaMemcpyHostToDevice, s0)) ||
-      (e = cudaMemcpyAsync(d_off, offp, (M + 1) * 8, cudaMemcpyHostToDevice, s0)) ||
+  if ((e = cudaMemcpyAsync(d_off, offp, (M + 1) * 8, cudaMemcpyHostToDevice, s0)) ||
       (e = cudaMemcpyAsync(d_perm, perm.data(), M * 4, cudaMemcpyHostToDevice, s0)) ||
       (e = cudaMemcpyAsync(d_soff, soff.data(), (M + 1) * 8, cudaMemcpyHostToDevice, s0)) ||
       (e = cudaMemcpyAsync(d_goff, goff.data(), goff.size() * 8, cudaMemcpyHostToDevice, s0)) ||
@@ -335,7 +380,6 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
                  n > 0) ? n : 148;
   }
   std::vector<cudaEvent_t> evs(chunks.size(), nullptr);
-  int64_t row_done = 0;
   int status = PCF_OK;
   bool one_mode = n_items > 0;
   for (int64_t i = 1; i < n_items && one_mode; ++i)
@@ -364,25 +408,29 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
     A.smem_mode = items[0].smem_mode;
     A.item_tag = (const int32_t*)d_tag;
     A.tag_done = (int32_t*)d_done;
+    if (timing) cudaEventRecord(tev[1], s0);
     if ((e = cudaMemsetAsync(d_cnt, 0, 4, s0)) || (e = launch_fill_tiles(A, s0)))
       return fail(e, "pcf_matrix_host fill");
+    if (timing) cudaEventRecord(tev[2], s0);
     single = true;
     for (size_t k = 0; k < chunks.size() && status == PCF_OK; ++k) {
-      // chunks alternate between two copy streams (more DMA in flight over PCIe)
+      // chunks alternate between two copy streams (more DMA in flight over PCIe); chunk
+      // k's rows need every chunk <= k finished: this stream already waited for k - 2 and
+      // k - 3, so it waits for k - 1 and k
       cudaStream_t sc = (k & 1) ? s2 : s1;
-      const unsigned n_k = (unsigned)(chunks[k].i1 - chunks[k].i0);
-      int r = wait((void*)sc, (unsigned long long)((int32_t*)d_done + k), n_k, 0 /*GEQ*/);
-      if (r) {
-        set_error("pcf_matrix_host: cuStreamWaitValue32 failed (%d)", r);
-        status = PCF_ERR_CUDA;
-        break;
+      for (size_t j = k > 0 ? k - 1 : 0; j <= k && status == PCF_OK; ++j) {
+        const unsigned n_j = (unsigned)(chunks[j].i1 - chunks[j].i0);
+        int r = wait((void*)sc, (unsigned long long)((int32_t*)d_done + j), n_j, 0 /*GEQ*/);
+        if (r) {
+          set_error("pcf_matrix_host: cuStreamWaitValue32 failed (%d)", r);
+          status = PCF_ERR_CUDA;
+        }
       }
-      if ((e = copy_rows(perm, row_done, chunks[k].row_end, (const char*)d_out, (char*)out, M,
-                         ld, es, sc))) {
+      if (status) break;
+      if ((e = copy_rows(perm, chunk_rows[k], (const char*)d_out, (char*)out, M, ld, es, sc))) {
         status = fail(e, "pcf_matrix_host drain");
         break;
       }
-      row_done = chunks[k].row_end;
     }
   }
   for (size_t k = 0; !single && k < chunks.size() && status == PCF_OK; ++k) {
@@ -402,11 +450,10 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
     if (status) break;
     if ((e = cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming)) ||
         (e = cudaEventRecord(evs[k], s0)) || (e = cudaStreamWaitEvent(s1, evs[k], 0)) ||
-        (e = copy_rows(perm, row_done, ch.row_end, (const char*)d_out, (char*)out, M, ld, es, s1))) {
+        (e = copy_rows(perm, chunk_rows[k], (const char*)d_out, (char*)out, M, ld, es, s1))) {
       status = fail(e, "pcf_matrix_host drain");
       break;
     }
-    row_done = ch.row_end;
   }
   unsigned long long key = ~0ull;
   cudaEvent_t join = nullptr;
@@ -415,7 +462,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
         (e = cudaEventRecord(join, s1)) || (e = cudaStreamWaitEvent(s0, join, 0)) ||
         (e = cudaEventRecord(join, s2)) || (e = cudaStreamWaitEvent(s0, join, 0)) ||
         (e = cudaMemcpyAsync(&key, d_err, 8, cudaMemcpyDeviceToHost, s0)) ||
-        (e = cudaStreamSynchronize(s0)))
+        (timing && (e = cudaEventRecord(tev[3], s0))) || (e = cudaStreamSynchronize(s0)))
       status = fail(e, "pcf_matrix_host sync");
     if (join) cudaEventDestroy(join);
   } else {
@@ -425,9 +472,21 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   }
   for (auto ev : evs)
     if (ev) cudaEventDestroy(ev);
-  if (timing)
-    fprintf(stderr, "pcf_matrix_host: host prep %.1f ms, total %.1f ms, %zu chunks, %lld items\n",
-            host_ms, ms_since(t_start), chunks.size(), (long long)n_items);
+  if (timing) {
+    fprintf(stderr, "pcf_matrix_host: host prep %.1f ms (sort %.1f, plan %.1f, order %.1f), "
+            "total %.1f ms, %zu chunks, %lld items\n", host_ms, sort_ms, plan_ms - sort_ms,
+            host_ms - plan_ms, ms_since(t_start), chunks.size(), (long long)n_items);
+    float up = 0.f, fill = 0.f, tail = 0.f;
+    if (single && status == PCF_OK) {
+      cudaEventElapsedTime(&up, tev[0], tev[1]);
+      cudaEventElapsedTime(&fill, tev[1], tev[2]);
+      cudaEventElapsedTime(&tail, tev[2], tev[3]);
+      fprintf(stderr, "pcf_matrix_host: device: upload+pack+diag %.1f ms, fill %.1f ms, "
+              "drain after fill %.1f ms\n", up, fill, tail);
+    }
+  }
+  for (auto ev : tev)
+    if (ev) cudaEventDestroy(ev);
   if (status) return status;
   if (key != ~0ull) {
     if (err_i) *err_i = (int64_t)(key / (unsigned long long)M);
