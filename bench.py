@@ -487,9 +487,10 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
             if bad is not None:
                 raise RuntimeError(f"non-finite entry {bad}")
         path = ("pcf_matrix_host (one C-ABI call): pinned host SoA (reference pack() layout) "
-                "-> H2D -> host size sort + plan -> pcf_pack_sorted -> diagonal + K1 fills in "
-                "32 cost-balanced chunks of size-sorted row blocks, each chunk's finished rows "
-                "D2H'd into the pinned M x M float64 result while later chunks compute")
+                "-> H2D (overlapped with the host size sort + plan) -> pcf_pack_sorted -> "
+                "diagonal -> one persistent K1 launch over a column-sweep queue in 512 "
+                "cost-balanced chunks; the rows each chunk finishes are D2H'd into the pinned "
+                "M x M float64 result on two copy streams while later chunks compute")
     elif shm is not None:
         path = ("pinned host SoA (reference pack() layout) -> H2D -> pcf_pack_sorted -> "
                 "pcf_fill_diagonal + pcf_fill_matrix (rank's share of the tile queue) -> "
