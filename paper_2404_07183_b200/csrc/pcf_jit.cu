@@ -283,7 +283,10 @@ int pcf_jit_load(const char* defs, void** module, char* log, int64_t logcap) {
     delete m;
     return drv_fail(r, "pcf_jit_load cuModuleGetFunction");
   }
-  if (g_drv.getfn(&m->single, m->mod, "pcf_jit_single")) m->single = nullptr;  // optional
+  // pcf_jit_single exists only for integrate_single definitions (PCF_HAS_U 1)
+  if (!strstr(defs, "#define PCF_HAS_U 1") ||
+      g_drv.getfn(&m->single, m->mod, "pcf_jit_single"))
+    m->single = nullptr;
   *module = m;
   return PCF_OK;
 }
