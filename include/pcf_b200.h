@@ -209,6 +209,7 @@ int pcf_jit_pairs(void* module, const void* recs_dev, const int64_t* soff_dev,
  * Fills the strict upper triangle of the plan's pairs, mirrored (the diagonal is the
  * caller's: pcf_jit_pairs on (s, s)); err_dev (init UINT64_MAX): atomicMin of the
  * (min, max) original-index key of the first non-finite / divergent entry. */
+int pcf_jit_tiles_cubin(const char* defs, int is_f32, int64_t* size, char* log, int64_t logcap);
 int pcf_jit_tiles_load(const char* defs, int is_f32, void** module, char* log, int64_t logcap);
 void pcf_jit_tiles_release(void* module);
 int pcf_jit_fill_tiles(void* module, int smem_mode, const void* recs_dev, const void* recsg_dev,

@@ -83,6 +83,7 @@ SIGNATURES = {
     "pcf_jit_cubin": (c_int, [ctypes.c_char_p, c_vp, c_i64, c_i64p, ctypes.c_char_p, c_i64]),
     "pcf_jit_load": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_vp), ctypes.c_char_p, c_i64]),
     "pcf_jit_release": (None, [c_vp]),
+    "pcf_jit_tiles_cubin": (c_int, [ctypes.c_char_p, c_int, c_i64p, ctypes.c_char_p, c_i64]),
     "pcf_jit_tiles_load": (c_int, [ctypes.c_char_p, c_int, ctypes.POINTER(c_vp), ctypes.c_char_p,
                                    c_i64]),
     "pcf_jit_tiles_release": (None, [c_vp]),

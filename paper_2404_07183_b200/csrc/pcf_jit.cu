@@ -291,6 +291,26 @@ int pcf_jit_load(const char* defs, void** module, char* log, int64_t logcap) {
   return PCF_OK;
 }
 
+int pcf_jit_tiles_cubin(const char* defs, int is_f32, int64_t* size, char* log, int64_t logcap) {
+  if (!defs || !size) {
+    set_error("pcf_jit_tiles_cubin: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  *size = 0;
+  const auto names = tiles_names(is_f32);
+  std::vector<char> cubin;
+  std::vector<std::string> low;
+  int rc = compile_src(tiles_source(defs, is_f32), names, &cubin, &low, log, logcap);
+  if (rc) return rc;
+  for (size_t k = 0; k < names.size(); ++k)
+    if (low[k].empty()) {
+      set_error("pcf_jit_tiles_cubin: no lowered name for %s", names[k].c_str());
+      return PCF_ERR_CUDA;
+    }
+  *size = (int64_t)cubin.size();
+  return PCF_OK;
+}
+
 int pcf_jit_tiles_load(const char* defs, int is_f32, void** module, char* log, int64_t logcap) {
   if (!defs || !module) {
     set_error("pcf_jit_tiles_load: bad arguments");

@@ -516,3 +516,17 @@ def compile_only(defs):
             f"device compilation failed ({lib.pcf_last_error().decode()}): "
             f"{log.value.decode(errors='replace')}")
     return size.value
+
+
+def compile_tiles_only(defs, f32=False):
+    """NVRTC-compile the tile kernels for a generated integrand without a GPU (CUBIN
+    size); every instantiation must be exported."""
+    lib = _native.load()
+    size = ctypes.c_int64(0)
+    log = ctypes.create_string_buffer(8192)
+    rc = lib.pcf_jit_tiles_cubin(defs.encode(), int(bool(f32)), ctypes.byref(size), log, 8192)
+    if rc != 0:
+        raise errors.UnsupportedIntegrand(
+            f"tile compilation failed ({lib.pcf_last_error().decode()}): "
+            f"{log.value.decode(errors='replace')}")
+    return size.value

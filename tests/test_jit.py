@@ -59,3 +59,28 @@ def test_unsupported_fail_loudly():
         jit.generate(h=h)
     h = eval("lambda x, y: np.maximum(x, y) * 2 - abs(y)", {"np": np})
     assert "pcf_npmax" in jit.generate(h=h)
+
+
+@pytest.mark.skipif(not _nvrtc_ok(), reason="NVRTC unavailable")
+@pytest.mark.parametrize("f32", [False, True])
+def test_tile_kernels_compile_for_user_integrands(f32):
+    """pcf_tiles.cuh (K1 / K1c / K1r / K1g) compiles under NVRTC with a user h and r and
+    exports all eight instantiations (pcf_jit_tiles_cubin)."""
+    defs = jit.generate(h=lambda x, y: abs(x - y) * (1.0 + x * y), r=math.sqrt)
+    assert jit.compile_tiles_only(defs, f32) > 0
+
+
+def test_symmetry_probe_and_tile_eligibility(monkeypatch):
+    from paper_2404_07183_b200.combine import (CombinationIntegral, _probably_symmetric,
+                                               _tiles_eligible)
+
+    assert _probably_symmetric(lambda x, y: abs(x - y))
+    assert _probably_symmetric(lambda x, y: x * y + min(x, y))
+    assert not _probably_symmetric(lambda x, y: x - 0.5 * y)
+    assert not _probably_symmetric(lambda x, y: math.log(x - y))  # raises on the probe set
+    sym = CombinationIntegral(h=lambda x, y: (x - y) ** 2, symmetric=True)
+    assert _tiles_eligible(sym)
+    assert not _tiles_eligible(CombinationIntegral(h=lambda x, y: (x - y) ** 2))
+    assert not _tiles_eligible(CombinationIntegral(H=lambda x, y, t: x * y * t, symmetric=True))
+    monkeypatch.setenv("PCF_JIT_NO_TILES", "1")
+    assert not _tiles_eligible(sym)
