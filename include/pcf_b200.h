@@ -59,7 +59,8 @@ typedef struct pcf_work_item {
   int32_t logC;      /* columns per streamed chunk = 1 << (logC & 0xff); bit 8: K1 streams
                         the columns through ONE buffer (twice the columns, half the G) */
   int32_t log2G;     /* merge-path segments per pair = 1 << log2G */
-  int32_t smem_mode; /* 1: K1 shared-memory tiles, 2: K1r one resident long row,
+  int32_t smem_mode; /* 1: K1 shared-memory tiles, 3: K1c one resident long row against
+                        streamed interleaved column groups, 2: K1r one resident long row,
                         0: K1g one lane per pair from L1/L2 (exact mode, long rows) */
   int32_t cost_hi;   /* estimated cells / 2^20 (scheduling order only) */
 } pcf_work_item;

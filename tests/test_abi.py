@@ -148,3 +148,21 @@ def test_no_cuda_means_loud_failure():
         pb.pdist(fs)
     with pytest.raises(errors.BackendUnavailable):
         pb.lp_distance(fs[0], fs[1])
+
+
+def test_jit_tile_prelude_matches_host_layout():
+    """The NVRTC prelude of the user-integrand tile module (csrc/pcf_jit.cu) restates
+    PcfWorkItem and kTileThreads; both must match the host definitions the planner fills
+    (include/pcf_b200.h, csrc/pcf_internal.h)."""
+    import re
+
+    hdr = open(os.path.join(ROOT, "include", "pcf_b200.h")).read()
+    body = re.search(r"typedef struct pcf_work_item \{(.*?)\} pcf_work_item;", hdr, re.S).group(1)
+    host_fields = re.findall(r"int32_t\s+(\w+);", body)
+    src = open(os.path.join(ROOT, "paper_2404_07183_b200", "csrc", "pcf_jit.cu")).read()
+    pre = re.search(r"struct PcfWorkItem \{ int ([^;]*); \};", src).group(1)
+    assert [f.strip() for f in pre.split(",")] == host_fields
+    internal = open(os.path.join(ROOT, "paper_2404_07183_b200", "csrc", "pcf_internal.h")).read()
+    n_host = re.search(r"constexpr int kTileThreads = (\d+);", internal).group(1)
+    n_rtc = re.search(r"constexpr int kTileThreads = (\d+);", src).group(1)
+    assert n_host == n_rtc
