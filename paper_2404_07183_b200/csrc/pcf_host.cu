@@ -217,11 +217,12 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   const double sort_ms = ms_since(t_start);
   int64_t n_items = 0;
   int32_t smem = 0;
-  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, 2048, max_log2G, rec_bytes, nullptr, 0,
+  static const int max_cols = getenv("PCF_HOST_MAX_COLS") ? atoi(getenv("PCF_HOST_MAX_COLS")) : 2048;
+  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, max_cols, max_log2G, rec_bytes, nullptr, 0,
                          &n_items, &smem);
   if (rc) return cudaStreamSynchronize(s0), rc;
   std::vector<pcf_work_item> items(n_items > 0 ? n_items : 1);
-  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, 2048, max_log2G, rec_bytes, items.data(),
+  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, max_cols, max_log2G, rec_bytes, items.data(),
                          n_items, &n_items, &smem);
   if (rc) return cudaStreamSynchronize(s0), rc;
   items.resize(n_items);
