@@ -159,3 +159,25 @@ def test_user_h_not_evaluated_on_tie_cells(monkeypatch):
     assert np.array_equal(np.asarray(pb.pairwise([f, g], ci, exact=False)), ref)
     ci2 = pb.CombinationIntegral(h=h, a=0.0, b=2.0, symmetric=True)  # b on a breakpoint
     assert np.array_equal(np.asarray(pb.pairwise([f, g], ci2)), one_thread(monkeypatch, [f, g], ci2))
+
+
+def test_tiny_collections_and_progress(monkeypatch):
+    """M = 1 (no tile items: the diagonal alone) and M = 2; progress sinks and
+    cancellation on the tile path behave as on the one-thread path."""
+    f = pb.make_pcf(np.array([[0.0, 1.5], [0.5, -2.0], [1.25, 0.0]]))
+    g = pb.make_pcf(np.array([[0.0, 0.25], [0.75, 0.0]]))
+    ci = pb.CombinationIntegral(h=sq_diff, r=math.sqrt, symmetric=True)
+    for fs in ([f], [f, g]):
+        assert np.array_equal(np.asarray(pb.pairwise(fs, ci)), one_thread(monkeypatch, fs, ci))
+    fs = collection(n=120)
+    job = pb.pairwise_job(fs, ci)
+    seen = []
+    job.subscribe(seen.append)
+    D = np.asarray(job.run())
+    assert seen[-1] == 1.0 and all(x <= y for x, y in zip(seen, seen[1:]))
+    assert np.array_equal(D, one_thread(monkeypatch, fs, ci))
+    assert job.entries_computed == len(fs) * (len(fs) + 1) // 2
+    job2 = pb.pairwise_job(fs, ci)
+    job2.cancel()
+    with pytest.raises(errors.Cancelled):
+        job2.run()
