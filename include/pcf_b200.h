@@ -165,13 +165,14 @@ int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* o
  * (pkg/src/pcflib/matrix.py:156-234 -> pack, fill_block per row block; pyx:72-121) in one
  * call.  tcat/vcat/off: the reference pack() layout in host memory (float64, or float32
  * when is_f32); out: host M x M (leading dimension ld) of the same kind, written in
- * original order (diagonal: exact 0 for LP, <f,f> for INNER when diag).  Device work runs
- * in n_chunks cost-balanced chunks of size-sorted row blocks; each chunk's finished rows
- * are copied to `out` on a second stream while later chunks compute (pin `out` with
- * cudaHostRegister / cudaMallocHost for the copies to overlap).  max_log2G as in
+ * original order (diagonal: exact 0 for LP, <f,f> for INNER when diag).  The work queue
+ * sweeps the column ranges right to left in max(n_chunks, 512) cost-balanced chunks; the
+ * rows each chunk finishes are copied to `out` on internal copy streams while later chunks
+ * compute (pin `out` with cudaHostRegister / cudaMallocHost for the copies to overlap).
+ * max_log2G as in
  * pcf_plan_pairwise.  *err_i/*err_j = -1, or the first (row-major, i < j) non-finite
- * pair.  Compute runs on `stream` (NULL: an internal stream), copies on an internal
- * stream joined back into it; synchronises before returning.  Device buffers are cached
+ * pair.  Compute runs on `stream` (NULL: an internal stream), copies on internal
+ * streams joined back into it; synchronises before returning.  Device buffers are cached
  * between calls (pcf_release_workspace frees them). */
 int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_t* off,
                     int64_t M, int op, double p, int apply_root, int diag, double a, double b,
