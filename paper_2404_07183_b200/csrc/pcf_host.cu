@@ -218,12 +218,16 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   int64_t n_items = 0;
   int32_t smem = 0;
   static const int max_cols = getenv("PCF_HOST_MAX_COLS") ? atoi(getenv("PCF_HOST_MAX_COLS")) : 2048;
-  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, max_cols, max_log2G, rec_bytes, nullptr, 0,
-                         &n_items, &smem);
-  if (rc) return cudaStreamSynchronize(s0), rc;
-  std::vector<pcf_work_item> items(n_items > 0 ? n_items : 1);
+  // one planner pass into a generous buffer (App-A 100k: 2.5 items per PCF); a second
+  // pass only if it was too small
+  std::vector<pcf_work_item> items((size_t)std::max<int64_t>(1024, 4 * M));
   rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, max_cols, max_log2G, rec_bytes, items.data(),
-                         n_items, &n_items, &smem);
+                         (int64_t)items.size(), &n_items, &smem);
+  if (rc == PCF_ERR_ARG && n_items > (int64_t)items.size()) {
+    items.resize((size_t)n_items);
+    rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, max_cols, max_log2G, rec_bytes,
+                           items.data(), n_items, &n_items, &smem);
+  }
   if (rc) return cudaStreamSynchronize(s0), rc;
   items.resize(n_items);
   const double plan_ms = ms_since(t_start);
