@@ -120,6 +120,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       getenv("PCF_SINGLE_MIN_LOG2G") ? atoi(getenv("PCF_SINGLE_MIN_LOG2G")) : 3;
   // largest G accepted for single-buffered K1 on rows whose group misses double buffering
   static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
+  static const bool kExactPartial = getenv("PCF_NO_EXACT_PARTIAL") == nullptr;
   static const int kSingleFallbackLogG =
       getenv("PCF_SINGLE_FALLBACK_LOG2G") ? atoi(getenv("PCF_SINGLE_FALLBACK_LOG2G")) : -1;
   std::vector<pcf_work_item> runs[4];  // by kernel: K1 (mode 1), K1c (3), K1r (2), K1g (0)
@@ -186,6 +187,36 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       }
     }
     bool single = false;
+    if (best_logRG < 0 && max_log2G == 0 && kExactPartial && (r0 % GW) == 0) {
+      // exact mode (G = 1): 64 columns per chunk do not fit next to this row block, so
+      // run K1 with idle quarters -- the most lanes (rows x columns) that fit, at least
+      // half the CTA, double-buffered when that keeps as many lanes -- instead of K1g
+      // (c2 exact, 200-record rows at 256 lanes: 30.8 -> 18.3 ms; App-A rows of 500+
+      // records reach only 64-128 lanes, which measured 1.8x slower than K1g)
+      constexpr int kExactMinLanes = kTileThreads / 2;
+      int best_lanes = 0;
+      for (int logRG = 1; logRG >= 0; --logRG) {
+        if (logRG == 1 && r0 + GW >= M - 1) continue;
+        int64_t rows_b = group_recs(r0) * RB;
+        if (logRG == 1) rows_b += group_recs(r0 + GW) * RB;
+        for (int nb = 2; nb >= 1; --nb)
+          for (int logC = LOGU - logRG; logC >= 2; --logC) {
+            const int64_t c0 = r0 + 1, ce = std::min<int64_t>(c0 + ((int64_t)1 << logC), M);
+            const int64_t need = al(rows_b) + nb * al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
+            if (need > smem_budget) continue;
+            const int lanes = (GW << logRG) << logC;
+            if (lanes >= kExactMinLanes && lanes > best_lanes) {
+              best_lanes = lanes;
+              best_logRG = logRG;
+              best_logC = logC;
+              best_logG = 0;
+              best_need = need;
+              single = nb == 1;
+            }
+            break;
+          }
+      }
+    }
     if (best_logRG < 0 && kSingleFallbackLogG >= 0 && (r0 % GW) == 0) {
       // the 8-row group fits only with ONE column buffer: K1 single-buffered at the
       // largest column count that fits (instead of K1r / K1g)

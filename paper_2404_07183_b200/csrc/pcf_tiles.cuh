@@ -270,7 +270,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const int cb = W.col0 + (c << logC);
       const int ce = min(cb + C, W.col1);
       const int qs = cb + cc;
-      const bool ok = row_ok && qs < ce && qs > ps;
+      // g >= G: an idle quarter (exact-mode items with fewer than 64 row x column lanes)
+      const bool ok = row_ok && qs < ce && qs > ps && g < G;
       mbar_wait(&bars[1 + kb], ph_col[kb]);
       ph_col[kb] ^= 1u;
       if (single && tid == 0 && c + 1 < nchunk) {
