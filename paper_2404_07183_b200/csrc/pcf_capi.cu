@@ -121,10 +121,11 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   // largest G accepted for single-buffered K1 on rows whose group misses double buffering
   static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
   static const bool kExactPartial = getenv("PCF_NO_EXACT_PARTIAL") == nullptr;
+  static const bool kK1sEnabled = getenv("PCF_NO_K1S") == nullptr;
   static const int kSingleFallbackLogG =
       getenv("PCF_SINGLE_FALLBACK_LOG2G") ? atoi(getenv("PCF_SINGLE_FALLBACK_LOG2G")) : -1;
-  std::vector<pcf_work_item> runs[4];  // by kernel: K1 (mode 1), K1c (3), K1r (2), K1g (0)
-  int64_t need_max = 0, k1r_need = 0, k1c_need = 0;
+  std::vector<pcf_work_item> runs[5];  // by kernel: K1 (mode 1), K1c (3), K1s (4), K1r (2), K1g (0)
+  int64_t need_max = 0, k1r_need = 0, k1c_need = 0, k1s_need = 0;
   const int64_t n_groups = (M + GW - 1) / GW;
   // K1c (one long row resident, interleaved column groups streamed): the best config for a
   // column range starting at group ks -- largest CG (fewest segments) that fits, double
@@ -237,7 +238,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       }
     }
     const bool smem = best_logRG >= 0 && (r0 % GW) == 0;
-    int rows, logC, logG;
+    int rows, logC, logG, s_mode = -1;
     if (smem && !single && best_logG >= kSingleMinLogG) {
       // long rows: G >= 16 merge-path segments of a few dozen steps each.  A single
       // column buffer of twice the columns halves G (half the co-rank searches and
@@ -267,6 +268,21 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       while (logG < std::min(max_log2G, 5) && (sizes[r0] >> (logG + 1)) >= 128) ++logG;
       logC = 9 - logG;
       k1r_need = std::max(k1r_need, al(sizes[r0] * RB));
+    } else if (max_log2G == 0 && kK1sEnabled && (r0 % GW) == 0 &&
+               al(group_recs(r0) * RB) <= smem_budget) {
+      // K1s (exact mode): the row block staged as in K1, columns through L1, 64 quarters
+      // = RG x C columns per pass
+      int64_t rows_b = group_recs(r0) * RB;
+      int lrg = 0;
+      if (r0 + GW < M - 1 && al(rows_b + group_recs(r0 + GW) * RB) <= smem_budget) {
+        rows_b += group_recs(r0 + GW) * RB;
+        lrg = 1;
+      }
+      rows = GW << lrg;
+      logG = 0;
+      logC = LOGU - lrg;
+      s_mode = 4;
+      k1s_need = std::max(k1s_need, al(rows_b));
     } else {  // rows too long for shared memory: operands from L1/L2 (K1g)
       logG = std::min(max_log2G, 5);
       const int P = T >> logG;
@@ -274,7 +290,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       logC = 0;
       while ((rows << (logC + 1)) <= P) ++logC;
     }
-    int mode = smem ? 1 : (rows == 1 ? 2 : 0);
+    int mode = smem ? 1 : (s_mode == 4 ? 4 : (rows == 1 ? 2 : 0));
     int64_t Rr = std::min<int64_t>(rows, M - r0);
     int64_t c_split = M;  // columns >= c_split of this row go to K1c
     if (mode == 2 && kK1cEnabled) {
@@ -330,7 +346,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       w.smem_mode = mode;
       const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;
       w.cost_hi = (int32_t)std::min(2.0e9, cells / 1048576.0);
-      runs[mode == 1 ? 0 : (mode == 2 ? 2 : 3)].push_back(w);
+      runs[mode == 1 ? 0 : (mode == 4 ? 2 : (mode == 2 ? 3 : 4))].push_back(w);
     }
     if (smem) need_max = std::max(need_max, best_need);
     r0 += Rr;
@@ -339,10 +355,11 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     return x.cost_hi > y.cost_hi;
   };
   for (auto& r : runs) std::stable_sort(r.begin(), r.end(), by_cost);
-  const int64_t total =
-      (int64_t)(runs[0].size() + runs[1].size() + runs[2].size() + runs[3].size());
+  int64_t total = 0;
+  for (auto& r : runs) total += (int64_t)r.size();
   *n_items = total;
-  if (smem_bytes) *smem_bytes = (int32_t)std::max(std::max(need_max, k1r_need), k1c_need);
+  if (smem_bytes)
+    *smem_bytes = (int32_t)std::max(std::max(need_max, k1r_need), std::max(k1c_need, k1s_need));
   if (items) {
     if (cap < total) {
       set_error("pcf_plan_pairwise: capacity %lld < %lld items", (long long)cap, (long long)total);

@@ -298,8 +298,8 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
       }
     for (int64_t x = 0; x < M; ++x) chunk_rows[owner[x] < 0 ? 0 : owner[x]].push_back((int32_t)x);
   }
-  // inside a chunk: one run per kernel (K1, K1c, K1r, K1g), each longest-first
-  auto mode_rank = [](int m) { return m == 1 ? 0 : (m == 3 ? 1 : (m == 2 ? 2 : 3)); };
+  // inside a chunk: one run per kernel (K1, K1c, K1s, K1r, K1g), each longest-first
+  auto mode_rank = [](int m) { return m == 1 ? 0 : (m == 3 ? 1 : (m == 4 ? 2 : (m == 2 ? 3 : 4))); };
   for (auto& ch : chunks) {
     std::stable_sort(items.begin() + ch.i0, items.begin() + ch.i1,
                      [&](const pcf_work_item& x, const pcf_work_item& y) {

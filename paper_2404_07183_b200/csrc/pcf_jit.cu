@@ -187,10 +187,10 @@ int compile_cubin(const char* defs, std::vector<char>* cubin, char* log, int64_t
 }
 
 // The tile kernels (K1, K1c, K1r, K1g) instantiated with HK = H_USER for one record kind,
-// both bound kinds: f[kernel][bounded], kernel 0 = K1, 1 = K1c, 2 = K1r, 3 = K1g.
+// both bound kinds: f[kernel][bounded], kernel 0 = K1, 1 = K1c, 2 = K1r, 3 = K1g, 4 = K1s.
 struct JitTiles {
   CUmodule mod = nullptr;
-  CUfunction f[4][2] = {};
+  CUfunction f[5][2] = {};
   int f32 = 0;
 };
 
@@ -223,6 +223,8 @@ std::vector<std::string> tiles_names(int f32) {
     snprintf(buf, sizeof buf, "pcfb::k_fill_rowres<5, %s, %s, %s>", bd, out, rec);
     v.push_back(buf);
     snprintf(buf, sizeof buf, "pcfb::k_fill_tiles_global<5, %s, %s, %s>", bd, out, rec);
+    v.push_back(buf);
+    snprintf(buf, sizeof buf, "pcfb::k_fill_rows_staged<5, %s, %s, %s, %s>", bd, out, rec, gw);
     v.push_back(buf);
   }
   return v;
@@ -336,13 +338,13 @@ int pcf_jit_tiles_load(const char* defs, int is_f32, void** module, char* log, i
     return drv_fail(r, "pcf_jit_tiles_load cuModuleLoadData");
   }
   for (int b = 0; b < 2; ++b)
-    for (int k = 0; k < 4; ++k) {
-      const std::string& ln = low[b * 4 + k];
+    for (int k = 0; k < 5; ++k) {
+      const std::string& ln = low[b * 5 + k];
       if (ln.empty() || (r = g_drv.getfn(&m->f[k][b], m->mod, ln.c_str()))) {
         g_drv.unload(m->mod);
         delete m;
         return r ? drv_fail(r, "pcf_jit_tiles_load cuModuleGetFunction")
-                 : (set_error("pcf_jit_tiles_load: no lowered name for %s", names[b * 4 + k].c_str()),
+                 : (set_error("pcf_jit_tiles_load: no lowered name for %s", names[b * 5 + k].c_str()),
                     PCF_ERR_CUDA);
       }
     }
@@ -365,8 +367,8 @@ int pcf_jit_fill_tiles(void* module, int smem_mode, const void* recs_dev, const 
   JitTiles* m = (JitTiles*)module;
   if (!m || !recs_dev || !soff_dev || !perm_dev || !items_dev || !counter_dev || !out_dev ||
       !err_dev || ld < M || !(a >= 0.0) || !(a < b) || n_items > 0x7fffffff ||
-      smem_mode < 0 || smem_mode > 3 || ((smem_mode == 1 || smem_mode == 3) &&
-                                         (!recsg_dev || !goff_dev))) {
+      smem_mode < 0 || smem_mode > 4 ||
+      ((smem_mode == 1 || smem_mode == 3 || smem_mode == 4) && (!recsg_dev || !goff_dev))) {
     set_error("pcf_jit_fill_tiles: bad arguments");
     return PCF_ERR_ARG;
   }
@@ -377,7 +379,8 @@ int pcf_jit_fill_tiles(void* module, int smem_mode, const void* recs_dev, const 
     set_error("pcf_jit_fill_tiles: %s", cudaGetErrorString(ce));
     return PCF_ERR_CUDA;
   }
-  const int kern = smem_mode == 1 ? 0 : (smem_mode == 3 ? 1 : (smem_mode == 2 ? 2 : 3));
+  const int kern = smem_mode == 1 ? 0
+                   : (smem_mode == 3 ? 1 : (smem_mode == 2 ? 2 : (smem_mode == 4 ? 4 : 3)));
   const int bounded = std::isinf(b) ? 0 : 1;
   CUfunction fn = m->f[kern][bounded];
   int dev = 0, nsm = 148;
@@ -394,7 +397,7 @@ int pcf_jit_fill_tiles(void* module, int smem_mode, const void* recs_dev, const 
   const void* null_tag = nullptr;
   void* null_done = nullptr;
   CUresult r;
-  if (kern <= 1) {
+  if (kern <= 1 || kern == 4) {
     void* args[] = {&recs_dev, &recsg_dev, &soff_dev, &goff_dev, &perm_dev, &items_dev, &n_,
                     &counter_dev, &p, &a, &b, &apply, &out_dev, &ld_, &M_, &err_dev, &null_tag,
                     &null_done};

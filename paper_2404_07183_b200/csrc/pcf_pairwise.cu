@@ -266,6 +266,25 @@ static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
           (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
           A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag, A.tag_done);
     }
+  } else if (A.smem_mode == 4) {  // K1s: exact mode, staged rows, columns through L1
+    cudaError_t e;
+    if (A.rec_bytes == 8) {
+      auto kern = k_fill_rows_staged<HK, BOUNDED, OutT, Rec32, 16>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+          (const Rec32*)A.recs, (const Rec32*)A.recs8, A.soff, A.goff8, A.perm, A.items,
+          A.n_items, A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err,
+          A.item_tag, A.tag_done);
+    } else {
+      auto kern = k_fill_rows_staged<HK, BOUNDED, OutT, Rec, 8>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+          (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
+          A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag,
+          A.tag_done);
+    }
   } else if (A.smem_mode == 3) {
     cudaError_t e;
     if (A.rec_bytes == 8) {

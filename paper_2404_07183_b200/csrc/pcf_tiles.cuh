@@ -500,6 +500,81 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 }
 
 // --------------------------------------------------------------------------------------
+// K1s: exact mode (G = 1) for row blocks whose 64 columns per chunk do not fit next to
+// them.  The row block is staged as in K1 (interleaved groups, one bulk copy); the
+// columns are read straight from global memory through L1.  Lanes as in K1: a
+// quarter-warp is the GW rows of a group against ONE column, so the 8 lanes of a quarter
+// read nearby records of the same column (few L1 lines per request) and conflict-free
+// rows.  64 quarters = RG x C columns per pass; no per-pass barrier (nothing streamed).
+template <int HK, bool BOUNDED, typename OutT, typename RT, int GW>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_fill_rows_staged(const RT* __restrict__ recs, const RT* __restrict__ recsg,
+                       const int64_t* __restrict__ soff, const int64_t* __restrict__ goff,
+                       const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
+                       int n_items, int* __restrict__ counter, double p, double a, double b,
+                       int apply_root, OutT* __restrict__ out, int64_t ld, int64_t M,
+                       unsigned long long* __restrict__ err,
+                       const int32_t* __restrict__ item_tag, int32_t* __restrict__ tag_done) {
+  constexpr int LOGGW = GW == 16 ? 4 : 3;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ int s_item;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t ph = 0;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= n_items) break;
+    const PcfWorkItem W = items[it];
+    const int logC = W.logC & 0xff;
+    const int logRG = W.nrows > GW ? 1 : 0;
+    const int RG = 1 << logRG, C = 1 << logC;
+    const int rg0 = W.row0 >> LOGGW;
+    const int64_t rbase = goff[rg0];
+    const uint32_t row_bytes = (uint32_t)((goff[rg0 + RG] - rbase) * sizeof(RT));
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bar, row_bytes);
+      bulk_g2s(smem, recsg + rbase, row_bytes, &bar);
+    }
+    const int u = tid & (GW - 1);
+    const int Q = tid >> LOGGW;
+    const int rho = Q & (RG - 1);
+    const int cc = (Q >> logRG) & (C - 1);
+    const int ps = W.row0 + GW * rho + u;
+    const bool row_ok = ps < M;
+    const RT* F = reinterpret_cast<const RT*>(smem) + (goff[rg0 + rho] - rbase) + u;
+    int nf = 0;
+    int64_t oi = 0;
+    if (row_ok) {
+      nf = (int)(soff[ps + 1] - soff[ps]);
+      oi = perm[ps];
+    }
+    mbar_wait(&bar, ph);
+    ph ^= 1u;
+    for (int cb = W.col0; cb < W.col1; cb += C) {
+      const int qs = cb + cc;
+      if (row_ok && qs < W.col1 && qs > ps) {
+        const RT* Gv = recs + soff[qs];
+        const int ng = (int)(soff[qs + 1] - soff[qs]);
+        const double acc = lane_walk<HK, BOUNDED, GW, 1, RT>(F, nf, Gv, ng, 0, 0, p, a, b);
+        const double hl = BOUNDED ? 0.0 : hval<HK>((double)F[(nf - 1) * GW].v,
+                                                   (double)Gv[ng - 1].v, p);
+        finish_entry<HK, BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
+      }
+    }
+    __syncthreads();  // every lane done with the rows before the next item's copy
+    if (tag_done && tid == 0) signal_item(item_tag, tag_done, it);
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // K1r: row-resident tiles for rows too long for K1's 8-row groups (the heavy tail of c4).
 //
 // A work item is ONE size-sorted row x a column range.  The row is loaded into shared

@@ -107,6 +107,12 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
         elif mode == 2:  # K1r: one resident row, C columns x G segments
             assert nrows == 1 and C * G == threads and G <= 32
             assert (sizes[row0] * rec_bytes + 127) // 128 * 128 <= smem <= 220 * 1024
+        elif mode == 4:  # K1s (exact mode): staged GW-row groups, columns through L1
+            assert max_log2g == 0 and G == 1 and row0 % gw == 0 and nrows <= 2 * gw
+            RG = 2 if nrows > gw else 1
+            assert RG * C == units
+            rows_b = sum(gw * sizes[row0 + gw * k] * rec_bytes for k in range(RG))
+            assert (rows_b + 127) // 128 * 128 <= smem <= 220 * 1024
         else:  # K1g: R x C pairs x G lanes in-warp (rows beyond shared memory)
             assert mode == 0 and nrows * C * G <= threads and G <= 32
             # rows beyond shared memory, or short rows that miss K1 (K1r is for >= 1024)
@@ -120,11 +126,11 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
     iu = np.triu_indices(M, 1)
     assert (seen[iu] == 1).all()
     assert seen.sum() == M * (M - 1) // 2
-    for m in (1, 3, 2, 0):
+    for m in (1, 3, 4, 2, 0):
         costs = items[items[:, 6] == m][:, 7]
         assert (np.diff(costs) <= 0).all()  # LPT order within each kernel's run
     runs = [m for k, m in enumerate(items[:, 6]) if k == 0 or items[k - 1, 6] != m]
-    assert runs == [m for m in (1, 3, 2, 0) if m in runs]  # one contiguous run per kernel
+    assert runs == [m for m in (1, 3, 4, 2, 0) if m in runs]  # one contiguous run per kernel
 
 
 def test_planner_rejects_unsorted():
