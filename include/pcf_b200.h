@@ -61,6 +61,7 @@ typedef struct pcf_work_item {
   int32_t log2G;     /* merge-path segments per pair = 1 << log2G */
   int32_t smem_mode; /* 1: K1 shared-memory tiles, 3: K1c one resident long row against
                         streamed interleaved column groups, 2: K1r one resident long row,
+                        4: K1s (exact mode) staged row groups, columns through L1,
                         0: K1g one lane per pair from L1/L2 (exact mode, long rows) */
   int32_t cost_hi;   /* estimated cells / 2^20 (scheduling order only) */
 } pcf_work_item;
@@ -203,7 +204,7 @@ int pcf_jit_matrix(void* module, const void* recs_dev, const int64_t* soff_dev,
 int pcf_jit_pairs(void* module, const void* recs_dev, const int64_t* soff_dev,
                   const int64_t* pairs_dev, int64_t npairs, double a, double b, int out_f32,
                   double* res_dev, int32_t* status_dev, void* stream);
-/* The tile kernels K1 / K1c / K1r / K1g (pcf_fill_matrix) instantiated for a user
+/* The tile kernels K1 / K1c / K1r / K1g / K1s (pcf_fill_matrix) instantiated for a user
  * integrand h (PCF_MODE 0, declared symmetric): NVRTC compiles csrc/pcf_tiles.cuh with
  * h in place of |x - y|^p and r in place of the p-th root, for one record kind
  * (is_f32: 8-byte float32 records, float output).  Replaces the per-rectangle Python

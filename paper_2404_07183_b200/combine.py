@@ -207,7 +207,7 @@ def _tiles_eligible(integral):
 
 
 def _fill_custom_tiles(coll, integral, out, exact, chunks, between):
-    """Symmetric pointwise integrands on the tile kernels (K1 / K1c / K1r / K1g compiled
+    """Symmetric pointwise integrands on the tile kernels (K1 / K1c / K1r / K1g / K1s compiled
     with h, pcf_jit_fill_tiles): strict upper triangle from the collection's work plan
     (exact: one lane per pair, the reference's left-to-right sum), diagonal by
     pcf_jit_pairs on (s, s).  Same return as fill_custom."""

@@ -1,6 +1,6 @@
-// Pairwise tile kernels (device code): the lane walk, the entry finisher and the four
+// Pairwise tile kernels (device code): the lane walk, the entry finisher and the five
 // persistent tile kernels K1 (k_fill_tiles_smem), K1c (k_fill_colgroups), K1g
-// (k_fill_tiles_global) and K1r (k_fill_rowres).  Included by pcf_pairwise.cu (nvcc, the
+// (k_fill_tiles_global), K1s (k_fill_rows_staged) and K1r (k_fill_rowres).  Included by pcf_pairwise.cu (nvcc, the
 // op-coded integrands) and compiled again at run time by NVRTC with a user integrand
 // (HK == H_USER, pcf_jit.cu) -- hence no host-only dependencies here.  See DESIGN.md.
 //

@@ -1,4 +1,4 @@
-"""User integrands on the tile kernels (pcf_jit_fill_tiles: K1 / K1c / K1r / K1g compiled
+"""User integrands on the tile kernels (pcf_jit_fill_tiles: K1 / K1c / K1r / K1g / K1s compiled
 by NVRTC with h and r in place of |x - y|^p and the p-th root).
 
 The one-thread-per-entry kernel (pcf_jit_matrix, bit-identical to the reference's cell

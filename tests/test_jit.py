@@ -64,8 +64,8 @@ def test_unsupported_fail_loudly():
 @pytest.mark.skipif(not _nvrtc_ok(), reason="NVRTC unavailable")
 @pytest.mark.parametrize("f32", [False, True])
 def test_tile_kernels_compile_for_user_integrands(f32):
-    """pcf_tiles.cuh (K1 / K1c / K1r / K1g) compiles under NVRTC with a user h and r and
-    exports all eight instantiations (pcf_jit_tiles_cubin)."""
+    """pcf_tiles.cuh (K1 / K1c / K1r / K1g / K1s) compiles under NVRTC with a user h and r and
+    exports all ten instantiations (pcf_jit_tiles_cubin)."""
     defs = jit.generate(h=lambda x, y: abs(x - y) * (1.0 + x * y), r=math.sqrt)
     assert jit.compile_tiles_only(defs, f32) > 0
 
