@@ -275,6 +275,8 @@ def run_ours(args):
                                               mode_runs, new_err, partition_items)
 
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if BACKEND != "nccl":  # ranks may share a GPU
         local = local % max(1, torch.cuda.device_count())
     if world > 1:
@@ -303,10 +305,12 @@ def run_ours(args):
     ev_k = []
 
     def step(record=False):
-        lib.pcf_fill_diagonal(_native.ptr(coll.recs), _native.ptr(coll.soff),
-                              _native.ptr(coll.perm), M, 0, 0.0, math.inf, _native.ptr(out), 0,
-                              M, _native.ptr(err), st)
-        launches = 1
+        launches = 0
+        if rank == 0:  # one writer per entry across ranks: the diagonal is rank 0's
+            lib.pcf_fill_diagonal(_native.ptr(coll.recs), _native.ptr(coll.soff),
+                                  _native.ptr(coll.perm), M, 0, 0.0, math.inf,
+                                  _native.ptr(out), 0, M, _native.ptr(err), st)
+            launches = 1
         for lo, hi, mode in mode_runs(my_items):
             cnt = hi - lo
             if record and mode == 1:
@@ -514,7 +518,8 @@ def run_e2e(args, t, v, off, pairs, world, rank, dev):
             items = (items_to_device(mine, dev), mine, smem)
         else:
             items = (items_dev, host_items, smem)
-        fill_pairwise(coll, 0, 1.0, True, False, out=out, items=items)
+        fill_pairwise(coll, 0, 1.0, True, False, out=out, items=items,
+                      diagonal=(rank == 0))
         if shm is not None:
             # every entry has exactly one writer and the buffers start at zero, so the
             # sum-reduce-scatter assembles each band exactly; each rank then drains its
@@ -588,6 +593,11 @@ def _shared_host_matrix(M, rank, world, dev):
     mm = None
     try:
         if rank == 0:
+            # a sparse file larger than the tmpfs would SIGBUS on first touch (the default
+            # container /dev/shm is 64 MB): check the free space first, fall back if short
+            st = os.statvfs("/dev/shm")
+            if st.f_bavail * st.f_frsize < M * M * 8 + (1 << 30):
+                raise OSError("not enough free space in /dev/shm")
             mm = np.memmap(path, dtype=np.float64, mode="w+", shape=(M, M))
     except (OSError, ValueError):
         ok[0] = 0
@@ -662,10 +672,38 @@ def _build_collection(coll, dt, dv, do, off_host, dev):
         _native.ptr(coll.recsg), current_stream_handle()), "pcf_pack_sorted")
 
 
+def _free_port():
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a torchrun environment: re-run this script as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1 and pass its exit
+    status through; rank 0 prints the JSON line."""
+    if args.impl == "ours" and BACKEND == "nccl":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) "
+                             "visible (NCCL needs one GPU per rank)\n")
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args)  # host cores only: rank 0 works, other ranks exit
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     else:
         run_ours(args)
 

@@ -40,10 +40,12 @@ def decode_err(err, M):
 
 
 def fill_pairwise(coll: DeviceCollection, op, p, apply_root, diag, a=0.0, b=math.inf,
-                  out=None, err=None, items=None, chunks=1, between_chunks=None, exact=False):
+                  out=None, err=None, items=None, chunks=1, between_chunks=None, exact=False,
+                  diagonal=True):
     """Write the full symmetric M x M matrix into `out` (device tensor, allocated if
-    None).  Diagonal: <f,f> when `diag` (Gram), exact 0 otherwise.  Returns
-    (out, err, stopped).  `items` = (items_dev, items_host, smem_bytes) or None for the
+    None).  Diagonal: <f,f> when `diag` (Gram), exact 0 otherwise; `diagonal=False`
+    leaves it untouched (the sharded recipe: only rank 0 owns the diagonal, so a sum
+    over the ranks' zero-initialised buffers stays exact).  Returns (out, err, stopped).  `items` = (items_dev, items_host, smem_bytes) or None for the
     collection's cached plan; `exact` selects the one-lane-per-pair plan.
     `between_chunks(frac)` is called after each of `chunks` slices of the queue has
     completed on the device; returning True stops early (cancellation)."""
@@ -63,10 +65,11 @@ def fill_pairwise(coll: DeviceCollection, op, p, apply_root, diag, a=0.0, b=math
         st = current_stream_handle()
         out_f32 = int(out.dtype == torch.float32)
         ld = out.stride(0)
-        _native.check(lib.pcf_fill_diagonal(
-            _native.ptr(coll.recs), _native.ptr(coll.soff), _native.ptr(coll.perm), M,
-            int(bool(diag)), float(a), float(b), _native.ptr(out), out_f32, ld,
-            _native.ptr(err), st), "pcf_fill_diagonal")
+        if diagonal:
+            _native.check(lib.pcf_fill_diagonal(
+                _native.ptr(coll.recs), _native.ptr(coll.soff), _native.ptr(coll.perm), M,
+                int(bool(diag)), float(a), float(b), _native.ptr(out), out_f32, ld,
+                _native.ptr(err), st), "pcf_fill_diagonal")
         counter = torch.zeros(1, dtype=torch.int32, device=dev)
         segs = []
         for base, end, mode in mode_runs(host_items):

@@ -136,10 +136,7 @@ def zeros(shape, dtype=np.float64) -> PcfArray:
     return PcfArray([z] * int(np.prod(shape)), shape=shape, dtype=dtype)
 
 
-def mean_along(array, dim) -> PcfArray:
-    """Mean PCF along `dim` (removed); a rank-1 input gives a 1-element array."""
-    from .reduce import mean_many
-
+def _fibres(array, dim):
     dim = int(dim)
     if dim < 0 or dim >= array.ndim:
         raise errors.BadDimension(f"dim {dim} out of range for rank {array.ndim}")
@@ -147,5 +144,22 @@ def mean_along(array, dim) -> PcfArray:
     out_shape = moved.shape[:-1] or (1,)
     fibres = [list(moved[ix]) for ix in np.ndindex(moved.shape[:-1])] if moved.ndim > 1 \
         else [list(moved)]
-    means = mean_many(fibres)
-    return PcfArray(means, shape=out_shape, dtype=array.dtype)
+    return fibres, out_shape
+
+
+def mean_along(array, dim) -> PcfArray:
+    """Mean PCF along `dim` (removed); a rank-1 input gives a 1-element array
+    (ndarray.py:241-265); every fibre in one batched device tree."""
+    from .reduce import mean_many
+
+    fibres, out_shape = _fibres(array, dim)
+    return PcfArray(mean_many(fibres), shape=out_shape, dtype=array.dtype)
+
+
+def std_along(array, dim, ddof=1) -> PcfArray:
+    """Pointwise sample std along `dim` (removed), pcflib.std per fibre
+    (reduce.py:236-238); every fibre in one batched device moments tree."""
+    from .reduce import std_many
+
+    fibres, out_shape = _fibres(array, dim)
+    return PcfArray(std_many(fibres, ddof=ddof), shape=out_shape, dtype=array.dtype)

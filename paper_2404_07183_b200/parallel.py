@@ -23,7 +23,8 @@ import math
 import numpy as np
 
 __all__ = ["subtree_blocks", "assemble_matrix", "gather_varlen", "mean_distributed",
-           "std_distributed"]
+           "std_distributed", "fill_pairwise_sharded", "matrix_distributed",
+           "partition_costs"]
 
 
 def subtree_blocks(M, world):
@@ -58,7 +59,8 @@ def gather_varlen(tensors, dst=0, group=None):
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    dev = tensors[0].device
+    # NCCL moves device tensors; gloo (host-side test plumbing) only host tensors
+    dev = torch.device("cpu") if dist.get_backend(group) == "gloo" else tensors[0].device
     n = torch.tensor([tensors[0].numel()], dtype=torch.int64, device=dev)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
@@ -67,11 +69,87 @@ def gather_varlen(tensors, dst=0, group=None):
     result = []
     for x in tensors:
         pad = torch.zeros(cap, dtype=x.dtype, device=dev)
-        pad[: x.numel()] = x
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad, group=group)
+        pad[: x.numel()] = x.to(dev)
+        # only dst receives payloads (the sizes went to everyone: 8 bytes per rank)
+        bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+        dist.gather(pad, bufs, dst=dst, group=group)
         result.append([b[:s] for b, s in zip(bufs, sizes)] if rank == dst else None)
     return result
+
+
+def partition_costs(host_items, sizes_sorted, world):
+    """Cells each rank computes under engine.partition_items (balance check)."""
+    from .engine import item_cells, partition_items
+
+    return [item_cells(partition_items(host_items, world, r), sizes_sorted)
+            for r in range(world)]
+
+
+def fill_pairwise_sharded(coll, op, p, apply_root, diag, a=0.0, b=math.inf, exact=False,
+                          group=None, out=None):
+    """This rank's share of the pairwise matrix: the collection's
+    cost-sorted work queue is dealt in snake order (engine.partition_items) and only
+    this rank's items run; rank 0 alone writes the diagonal (Gram <f,f> or the distance
+    zeros), so every entry of the M x M matrix has exactly one writer across the ranks.
+    `out` (device, zero-initialised if None) receives only the rank's entries; summing
+    the ranks' buffers (assemble_matrix, or a reduce-scatter) gives the single-GPU
+    matrix bit for bit.  Returns (out, err) with err the engine's first-failure word."""
+    import torch
+    import torch.distributed as dist
+
+    from .engine import fill_pairwise, items_to_device, partition_items
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    _, host_items, smem = coll.plan(exact=exact)
+    mine = partition_items(host_items, world, rank)
+    if out is None:
+        out = torch.zeros((coll.M, coll.M), dtype=coll.out_torch_dtype, device=coll.device)
+    out, err, _ = fill_pairwise(coll, op, p, apply_root, diag, a, b, out=out,
+                                items=(items_to_device(mine, coll.device), mine, smem),
+                                exact=exact, diagonal=(rank == 0))
+    return out, err
+
+
+def _min_err_word(err, group):
+    """Minimum over ranks of the engine's unsigned first-failure words (UINT64_MAX =
+    none): flip the sign bit so a signed MIN orders them as unsigned."""
+    import torch
+    import torch.distributed as dist
+
+    flip = -(1 << 63)
+    key = err.to(torch.int64) ^ flip
+    on_host = dist.get_backend(group) == "gloo"
+    buf = key.cpu() if on_host else key
+    dist.all_reduce(buf, op=dist.ReduceOp.MIN, group=group)
+    return buf.to(err.device) ^ flip
+
+
+def matrix_distributed(tcat, vcat, off, op, p, apply_root, diag, a=0.0, b=math.inf,
+                       exact=False, device=None, group=None, dst=0):
+    """Whole pairwise matrix over all ranks of `group`: every rank packs the collection,
+    computes its share (fill_pairwise_sharded) and C1 sum-reduces the buffers onto
+    `dst`.  Returns (matrix, first_failing_pair) on dst, (None, None) elsewhere; the
+    failing pair is the minimum over the ranks (the row-major first, as the reference
+    reports it)."""
+    import torch.distributed as dist
+
+    from .collection import DeviceCollection
+    from .engine import decode_err
+
+    coll = DeviceCollection(tcat, vcat, off, device=device)
+    out, err = fill_pairwise_sharded(coll, op, p, apply_root, diag, a, b, exact, group)
+    err_min = _min_err_word(err, group)
+    if dist.get_backend(group) == "gloo":  # gloo reduces host tensors only
+        host = out.cpu()
+        dist.reduce(host, dst=dst, group=group)
+        if dist.get_rank(group) == dst:
+            out.copy_(host)
+    else:
+        assemble_matrix(out, group=group, dst=dst)
+    if dist.get_rank(group) != dst:
+        return None, None
+    return out, decode_err(err_min, coll.M)
 
 
 def _local_level(tcat, vcat, off, lo, hi, device):

@@ -93,9 +93,10 @@ class DeviceLevel:
 
     def to_pcfs(self, values=None):
         """Host Pcf objects, one per node."""
-        t = self.t.cpu().numpy()
-        v = (self.v if values is None else values).cpu().numpy()
-        off = self.off.cpu().numpy()
+        n = self.ntot  # buffers may be scratch capacity: copy only the live points
+        t = self.t[:n].cpu().numpy()
+        v = (self.v if values is None else values)[:n].cpu().numpy()
+        off = self.off[: self.nnodes + 1].cpu().numpy()
         out = []
         for k in range(self.nnodes):
             mat = np.empty((off[k + 1] - off[k], 2), dtype=t.dtype)
@@ -379,6 +380,19 @@ def mean_many(fibres):
     flat = [g for f in fibres for g in f]
     level = DeviceLevel.from_pcfs(flat)
     return mean_packed(level, [len(f) for f in fibres]).to_pcfs()
+
+
+def std_many(fibres, ddof=1, take_sqrt=True):
+    """Stds (or variances) of several independent collections in one batched device
+    moments tree (segmented by fibre, like mean_many)."""
+    fibres = [list(f) for f in fibres]
+    for f in fibres:
+        if len(f) < 2:
+            raise errors.InsufficientData("variance needs at least two PCFs")
+    flat = [g for f in fibres for g in f]
+    level = DeviceLevel.from_pcfs(flat)
+    return std_packed(level, ddof, take_sqrt=take_sqrt,
+                      seg_nodes=[len(f) for f in fibres]).to_pcfs()
 
 
 def _moments_level(level: DeviceLevel):

@@ -137,3 +137,27 @@ def test_aligned_subtrees_reproduce_full_tree(M, world):
     full = O.minimize(_tree_raw(mats))
     parts = [_tree_raw(mats[lo:hi]) for lo, hi in parallel.subtree_blocks(M, world) if hi > lo]
     assert np.array_equal(O.minimize(_tree_raw(parts)), full)
+
+
+def test_c3_partition_cost_balanced():
+    """The snake deal of the c3 plan (100k App-A PCFs, RngSpec(2404)) gives every one of
+    2/4/8 ranks the same number of rectangle cells to within 2% (max/min), in both the
+    fast and the exact plan."""
+    t, v, off = dg.synthetic_benchmark_packed(100000, rng=dg.RngSpec(2404))
+    sizes = np.diff(off)
+    ss = np.ascontiguousarray(sizes[np.argsort(-sizes, kind="stable")], dtype=np.int64)
+    lib = _native.load()
+    total = (len(ss) - 1) * int(ss.sum()) - len(ss) * (len(ss) - 1) // 2
+    for log2g in (6, 0):
+        n, smem = ctypes.c_int64(), ctypes.c_int32()
+        lib.pcf_plan_pairwise(_native.ptr(ss), ss.shape[0], 220 * 1024, 2048, log2g, 16, None,
+                              0, ctypes.byref(n), ctypes.byref(smem))
+        items = (_native.WorkItem * n.value)()
+        lib.pcf_plan_pairwise(_native.ptr(ss), ss.shape[0], 220 * 1024, 2048, log2g, 16,
+                              ctypes.cast(items, ctypes.c_void_p), n.value, ctypes.byref(n),
+                              ctypes.byref(smem))
+        host = np.frombuffer(items, dtype=np.int32).reshape(-1, 8)[: n.value].copy()
+        for world in (2, 4, 8):
+            costs = parallel.partition_costs(host, ss, world)
+            assert sum(costs) == total  # every pair exactly once
+            assert max(costs) / min(costs) <= 1.02, (log2g, world, costs)

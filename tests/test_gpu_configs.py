@@ -1,0 +1,218 @@
+"""Config-scale parity (BASELINE.json configs c1-c5 at their full sizes) on the B200.
+
+Checked against the reference's own compiled kernel (oracle/_ref: _sweepkern.pyx built
+from the reference source; the C restatement when absent) on sampled rows, or against
+brute-force pointwise evaluation for the 1e6-PCF reductions -- the reference's
+acceptance checks (tests/test_acceptance.py:51-111) at the configs' sizes.
+Bitwise where the design promises it (exact plan: one lane per pair, reference sum
+order; p = 1 and Gram), else the north-star tolerance: relative 1e-12 (float64), 1e-5
+(float32), Gram entries condition-aware |d| <= tol * sqrt(K_ii K_jj).
+"""
+
+import math
+import os
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a GPU")]
+
+import oracle as O  # noqa: E402
+from paper_2404_07183_b200 import datagen as dg  # noqa: E402
+from paper_2404_07183_b200.collection import DeviceCollection  # noqa: E402
+from paper_2404_07183_b200.engine import decode_err, fill_pairwise, mode_runs  # noqa: E402
+
+
+def ref_rows(t, v, off, rows, op, p, root, diag=False):
+    """D[i, :] rows of the reference kernel (fill_block(i, i + 1) into an O(M) aliasing
+    sink leaves D[i, i+1:] in buf[i+1:]), all host threads."""
+    from numpy.lib.stride_tricks import as_strided
+
+    K = O.load_reference_kernel()
+    M = off.shape[0] - 1
+    res, todo, lock = {}, list(rows), threading.Lock()
+    orc = O.Oracle() if K is None else None
+
+    def work():
+        buf = np.zeros(M, dtype=t.dtype)
+        sink = as_strided(buf, shape=(M, M), strides=(0, buf.itemsize))
+        while True:
+            with lock:
+                if not todo:
+                    return
+                i = todo.pop()
+            if K is not None:
+                K.fill_block((t, v, off), i, i + 1, op, p, root, diag, 0.0, math.inf, sink)
+                row = buf.copy()
+            else:
+                row = orc.row(t.astype(np.float64), v.astype(np.float64), off, i, op, p,
+                              root).astype(t.dtype)
+            with lock:
+                res[i] = row
+
+    ths = [threading.Thread(target=work) for _ in range(min(len(rows), os.cpu_count() or 1))]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    return res
+
+
+def ref_diag(t, v, off, rows):
+    orc = O.Oracle()
+    out = {}
+    for i in rows:
+        f = np.column_stack((t[off[i]:off[i + 1]], v[off[i]:off[i + 1]])).astype(np.float64)
+        out[i] = orc.accumulate(f, f, op=1, p=0.0)
+    return out
+
+
+def rel(x, ref):
+    x, ref = x.astype(np.float64), ref.astype(np.float64)
+    return float(np.max(np.abs(x - ref) / np.maximum(np.abs(ref), 1e-300)))
+
+
+def fill(coll, op, p, root, diag, exact, out=None):
+    out, err, _ = fill_pairwise(coll, op, p, root, diag, out=out, exact=exact)
+    assert decode_err(err, coll.M) is None
+    return out
+
+
+def test_c1_full_matrix_both_plans():
+    t, v, off = dg.pack_matrices(dg.fixed_size_collection(1000, 100))
+    ref, bad = O.Oracle().matrix(t, v, off, op=0, p=1.0)
+    assert bad is None
+    coll = DeviceCollection(t, v, off)
+    D = fill(coll, 0, 1.0, True, False, exact=True).cpu().numpy()
+    assert np.array_equal(D, ref)
+    D = fill(coll, 0, 1.0, True, False, exact=False).cpu().numpy()
+    assert rel(D, ref) < 1e-12 and np.array_equal(D, D.T)
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-12), (np.float32, 1e-5)])
+def test_c2_gram_10k(dtype, tol):
+    M = 10000
+    t, v, off = dg.pack_matrices(dg.fixed_size_collection(M, 200, dtype=dtype))
+    rows = sorted(set(np.linspace(0, M - 2, 32).astype(int)) | {0, M - 2})
+    ref = ref_rows(t, v, off, rows, 1, 0.0, False, diag=True)
+    dref = ref_diag(t, v, off, rows)
+    coll = DeviceCollection(t, v, off)
+    buf = None
+    for exact in (True, False):
+        buf = fill(coll, 1, 0.0, False, True, exact, out=buf)
+        K = buf.cpu().numpy()
+        assert K.dtype == dtype
+        kd = np.sqrt(np.abs(np.diag(K).astype(np.float64)))
+        for i in rows:
+            got, want = K[i, i + 1:], ref[i][i + 1:]
+            assert K[i, i] == dtype(dref[i])  # the diagonal walk is always sequential
+            if exact:
+                assert np.array_equal(got, want), i
+            else:
+                d = np.abs(got.astype(np.float64) - want) / np.maximum(kd[i] * kd[i + 1:],
+                                                                      1e-300)
+                assert float(d.max()) < tol, (i, float(d.max()))
+
+
+@pytest.mark.parametrize("p", [2.0, 3.0])
+def test_c4_heavy_tail_lp(p):
+    M = 10000
+    t, v, off = dg.pack_matrices(dg.ecc_like_collection(M))
+    sizes = np.diff(off)
+    longest = list(np.argsort(-sizes, kind="stable")[:8])  # K1c / K1r rows
+    rows = sorted(set(int(r) for r in longest) | set(np.linspace(0, M - 2, 10).astype(int)))
+    rows = [r for r in rows if r < M - 1]
+    ref = ref_rows(t, v, off, rows, 0, p, True)
+    coll = DeviceCollection(t, v, off)
+    _, host, _ = coll.plan(exact=False)
+    kinds = {m for _, _, m in mode_runs(host)}
+    assert {1, 2, 3} <= kinds, kinds  # K1, K1r and K1c all carry work at c4
+    D = fill(coll, 0, p, True, False, exact=False).cpu().numpy()
+    worst = max(rel(D[i, i + 1:], ref[i][i + 1:]) for i in rows)
+    assert worst < 1e-12, worst
+    assert np.array_equal(D, D.T)
+
+
+def test_c3_rows_exact_bitwise_and_fast():
+    """100k App-A PCFs (pcflib.synthetic_benchmark(100000, RngSpec(2404))): 4 full rows
+    bit-identical to the reference kernel in the exact plan, within 1e-12 in the fast
+    plan (the bench's headline plan)."""
+    import torch
+
+    M = 100000
+    t, v, off = dg.synthetic_benchmark_packed(M, rng=dg.RngSpec(2404))
+    rows = [1, M // 3, (2 * M) // 3, M - 2]
+    ref = ref_rows(t, v, off, rows, 0, 1.0, True)
+    coll = DeviceCollection(t, v, off)
+    buf = torch.empty((M, M), dtype=torch.float64, device=coll.device)
+    for exact in (True, False):
+        fill(coll, 0, 1.0, True, False, exact, out=buf)
+        for i in rows:
+            got = buf[i].cpu().numpy()
+            assert got[i] == 0.0
+            if exact:
+                assert np.array_equal(got[i + 1:], ref[i][i + 1:]), i
+            else:
+                assert rel(got[i + 1:], ref[i][i + 1:]) < 1e-12, i
+            # symmetric: the mirror column carries the same values
+            assert np.array_equal(buf[:, i].cpu().numpy(), got)
+    del buf
+    torch.cuda.empty_cache()
+
+
+def test_c5_mean_std_1e6():
+    """mean/std of 1e6 noisy-sine PCFs (101 points) vs brute-force pointwise evaluation
+    of all 1e6 PCFs at 256 probe times (test_acceptance.py:71-87)."""
+    import torch
+
+    from paper_2404_07183_b200.reduce import DeviceLevel, mean_packed, std_packed
+
+    M = 1000000
+    _, mats = dg.noisy_trig_matrices((M,), 100, "sin", 0.1, dg.RngSpec(2404))
+    t, v, off = dg.pack_matrices(mats)
+    del mats
+    lvl = DeviceLevel.from_packed(t, v, off)
+    m, s = mean_packed(lvl), std_packed(lvl)
+    T = torch.from_numpy(t.reshape(M, 101))
+    V = torch.from_numpy(v.reshape(M, 101))
+    probes = np.sort(np.random.default_rng(0).uniform(0, 1, 256))
+    P = torch.from_numpy(probes).expand(M, 256).contiguous()
+    vals = torch.gather(V, 1, torch.searchsorted(T, P, right=True) - 1).numpy()
+    mu = vals.sum(0) / M
+    sd = np.sqrt(((vals - vals.mean(0)) ** 2).sum(0) / (M - 1))
+    mt, mv = m.t[: m.ntot].cpu().numpy(), m.v[: m.ntot].cpu().numpy()
+    st, sv = s.t[: s.ntot].cpu().numpy(), s.v[: s.ntot].cpu().numpy()
+    gm = mv[np.searchsorted(mt, probes, side="right") - 1]
+    gs = sv[np.searchsorted(st, probes, side="right") - 1]
+    assert float(np.max(np.abs(gm - mu) / np.maximum(np.abs(mu), 1.0))) < 1e-12
+    assert float(np.max(np.abs(gs - sd) / sd)) < 1e-12
+    assert mt[0] == 0.0 and st[0] == 0.0 and (np.diff(mt) > 0).all()
+    # minimal discretisation (the reference's final minimise)
+    assert (mv[1:] != mv[:-1]).all() and (sv[1:] != sv[:-1]).all()
+
+
+def test_masspcf_std_matches_reference_goldens(golden):
+    """Frontend std (batched moments tree over the fibres of an array) vs pcflib.std."""
+    import paper_2404_07183_b200 as pb
+    from conftest import unpack
+    from paper_2404_07183_b200 import masspcf as mpcf
+
+    fs = [pb.make_pcf(x) for x in unpack(golden, "sin64")]
+    n = len(fs)
+    A = mpcf.zeros((2, n))
+    A[0, :] = fs
+    A[1, :] = fs[::-1]
+    S = mpcf.std(A, dim=1)
+    assert tuple(S.shape) == (2,)
+    want = golden["sin64_std"]
+    for r in range(2):
+        got = np.asarray(S[r])
+        ts = np.union1d(got[:, 0], want[:, 0])
+        a = got[np.searchsorted(got[:, 0], ts, side="right") - 1, 1]
+        b = want[np.searchsorted(want[:, 0], ts, side="right") - 1, 1]
+        assert float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))) < 1e-12
+    S0 = mpcf.std(A, dim=0)  # 2-element fibres
+    assert tuple(S0.shape) == (n,)
