@@ -6,10 +6,12 @@
  *
  *   _Backend.integrate_pair(f, g, a, b, op, p)  _backend.py:31-38 -> pcf_integrate_pair_host
  *       (= _sweepkern.integrate_pair, _sweepkern.pyx:62-69)
- *   _Backend.pack(collection)                   _backend.py:40-41 -> pcf_pack_sorted (device)
- *       (= _sweepkern.pack, _sweepkern.pyx:72-85; host concat stays in the caller)
- *   _Backend.fill_block(packed, r0, r1, ...)    _backend.py:43-46 -> pcf_fill_rows (device) /
- *       pcf_fill_block_host (host buffers)     (= _sweepkern.fill_block, pyx:88-121)
+ *   _Backend.pack(collection)                   _backend.py:40-41 -> pcf_collection_create
+ *       (= _sweepkern.pack, _sweepkern.pyx:72-85; device-resident, size-sorted handle;
+ *        pcf_pack_sorted is the device-pointer form)
+ *   _Backend.fill_block(packed, r0, r1, ...)    _backend.py:43-46 -> pcf_collection_fill_block
+ *       (= _sweepkern.fill_block, pyx:88-121; pcf_fill_rows / pcf_fill_block_host are the
+ *        device-pointer and stateless host forms)
  *
  * plus the whole-matrix path the GPU needs (MatrixJob.run's block loop,
  * pkg/src/pcflib/matrix.py:156-234, moved on-device): pcf_plan_pairwise + pcf_fill_matrix,
@@ -49,6 +51,10 @@ extern "C" {
 
 #define PCF_OP_LP 0
 #define PCF_OP_INNER 1
+/* Flag or'ed into op: L_p cells with p != 1 may use d*d, d*d*|d| or CUDA's pow instead of
+ * the default, the C library's pow restated bit for bit (csrc/pcf_pow.cuh), which makes
+ * every p bitwise equal to the reference in the exact plan.  Roots always use the latter. */
+#define PCF_OP_FAST_POW 0x10
 
 /* One work item of the pairwise tile scheduler (32 bytes, device-resident array). */
 typedef struct pcf_work_item {
@@ -162,6 +168,28 @@ int pcf_fill_block_host(const double* tcat, const double* vcat, const int64_t* o
                         double a, double b, double* out, int64_t ld, int64_t* err_i,
                         int64_t* err_j);
 
+/* ---- kernel-plugin handle: _Backend.pack / fill_block (pkg/src/pcflib/_backend.py:40-46,
+ * _sweepkern.pack / fill_block pyx:72-121) for a plugin inside the reference's MatrixJob
+ * (matrix.py:169-227: pack once, fill_block on disjoint row blocks from many threads).
+ * pcf_collection_create uploads the pack() layout (tcat/vcat float64, or float32 when
+ * is_f32; off int64[M+1]) once and packs it size-sorted on the current device.
+ * pcf_collection_fill_block writes rows [r0, r1) (j >= i with diag, else j > i) and their
+ * mirrors into the host matrix `out` (float64, or float32 when out_is_f32; leading
+ * dimension ld) exactly as _sweepkern.fill_block does: returns with *err_i/*err_j = the
+ * block's first non-finite entry in row-major order (-1 if none), entries after it
+ * untouched.  The first call for a given (op, p, apply_root, diag, a, b, max_log2G)
+ * computes the whole matrix on the device with the tile kernels and caches it on the
+ * handle (float64); every call copies its rows from that cache.  max_log2G 0 = exact plan
+ * (bitwise equal to pcf_integrate_pair_host and to the reference for every p), > 0 = fast
+ * plan.  Thread-safe: concurrent fill_block calls on one handle are allowed. */
+int pcf_collection_create(const void* tcat, const void* vcat, int is_f32, const int64_t* off,
+                          int64_t M, void** handle);
+void pcf_collection_free(void* handle);
+int pcf_collection_fill_block(void* handle, int64_t r0, int64_t r1, int op, double p,
+                              int apply_root, int diag, double a, double b, int32_t max_log2G,
+                              void* out, int out_is_f32, int64_t ld, int64_t* err_i,
+                              int64_t* err_j);
+
 /* Whole matrix from host buffers (serialised per process): MatrixJob.run over the compiled module
  * (pkg/src/pcflib/matrix.py:156-234 -> pack, fill_block per row block; pyx:72-121) in one
  * call.  tcat/vcat/off: the reference pack() layout in host memory (float64, or float32
@@ -224,6 +252,13 @@ int pcf_jit_fill_tiles(void* module, int smem_mode, const void* recs_dev, const 
 int pcf_jit_single(void* module, const void* recs_dev, const int64_t* soff_dev, int64_t M,
                    double a, double b, int out_f32, double* res_dev, int32_t* status_dev,
                    void* stream);
+
+/* out[i] = pow(x[i], y[i]) with the device restatement of the C library's pow that every
+ * L_p kernel uses (csrc/pcf_pow.cuh; bit-identical to glibc 2.39 libm pow, the reference's
+ * pow at _sweepkern.pyx:43-46,98,114).  For verification and for host callers that want
+ * the same rounding on the device. */
+int pcf_pow_batch(const double* x_dev, const double* y_dev, int64_t n, double* out_dev,
+                  void* stream);
 
 /* Dense FP64 FMA throughput probe: nsm*blocks_per_sm CTAs x 256 threads x 8 chains x iters
  * DFMA (2 flops each); time it with events on `stream` for the FP64 roofline. */

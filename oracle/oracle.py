@@ -42,7 +42,7 @@ def build(ref=True):
     """make -C oracle [ref]; the ref target needs /root/reference (this container)."""
     subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
     if ref and os.path.exists("/root/reference/pkg/src/pcflib/_sweepkern.pyx"):
-        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", HERE, "ref", "refpkg"], check=True)
 
 
 class Oracle:

@@ -43,36 +43,76 @@ class _Backend:
         return res.value
 
     def pack(self, collection):
-        """Device-resident packed collection (see collection.DeviceCollection)."""
-        from .collection import DeviceCollection
+        """Device-resident, size-sorted copy of the collection (pcf_collection_create):
+        the reference's packed tuple (_sweepkern.pack, pyx:72-85) as an opaque handle."""
+        return PackedHandle(collection)
 
-        return DeviceCollection.from_pcfs(collection)
-
-    def fill_block(self, packed, r0, r1, op, p, apply_root, diag, a, b, out):
+    def fill_block(self, packed, r0, r1, op, p, apply_root, diag, a, b, out, exact=True):
         """Rows [r0, r1) of the symmetric matrix into host array `out` (mirrored);
         returns None or the first non-finite (i, j) -- entries after it in the block
-        are left untouched, as in the reference."""
-        from .engine import decode_err, fill_rows
-
-        M = packed.M
-        slab, err = fill_rows(packed, r0, r1, op, p, apply_root, diag, a, b,
-                              out_f32=(np.dtype(out.dtype) == np.float32))
-        host = slab.cpu().numpy()
-        bad = decode_err(err, M)
-        for i in range(r0, r1):
-            j0 = i if diag else i + 1
-            if bad is not None and bad[0] == i:
-                row = host[i - r0, j0:bad[1]]
-                out[i, j0:bad[1]] = row
-                out[j0:bad[1], i] = row
-                return bad
-            row = host[i - r0, j0:]
-            out[i, j0:] = row
-            out[j0:, i] = row
-        return None
+        are left untouched, as in the reference (pyx:88-121).  The first block of a job
+        computes the whole matrix on the device (tile kernels; exact plan by default, so
+        entries equal integrate_pair bit for bit) and caches it on the handle."""
+        if not isinstance(packed, PackedHandle):
+            packed = PackedHandle(packed)
+        return packed.fill_block(r0, r1, op, p, apply_root, diag, a, b, out, exact)
 
     def __repr__(self):
         return f"<kernel backend: {self.name}>"
+
+
+class PackedHandle:
+    """pcf_collection_create handle for a list of Pcf (or an (tcat, vcat, off) tuple in
+    the reference pack() layout); freed with the object."""
+
+    def __init__(self, collection):
+        import ctypes
+
+        from .collection import require_cuda
+        from .datagen import pack_matrices
+
+        require_cuda()
+        self._lib = _native.load()
+        self._h = None
+        if isinstance(collection, tuple) and len(collection) == 3:
+            tcat, vcat, off = collection
+        else:
+            coll = list(collection)
+            if not coll:
+                raise errors.EmptyCollection("empty collection")
+            kind = coll[0].dtype
+            if any(f.dtype != kind for f in coll):
+                raise errors.MixedPrecision("collection mixes 32- and 64-bit PCFs")
+            tcat, vcat, off = pack_matrices([f.to_matrix() for f in coll], kind)
+        self.tcat = np.ascontiguousarray(tcat)
+        self.vcat = np.ascontiguousarray(vcat, dtype=self.tcat.dtype)
+        self.off = np.ascontiguousarray(off, dtype=np.int64)
+        self.M = int(self.off.shape[0] - 1)
+        h = ctypes.c_void_p()
+        _native.check(self._lib.pcf_collection_create(
+            _native.ptr(self.tcat), _native.ptr(self.vcat), int(self.tcat.dtype == np.float32),
+            _native.ptr(self.off), self.M, ctypes.byref(h)), "pcf_collection_create")
+        self._h = h
+
+    def fill_block(self, r0, r1, op, p, apply_root, diag, a, b, out, exact=True):
+        import ctypes
+
+        if not (isinstance(out, np.ndarray) and out.ndim == 2 and out.flags.c_contiguous and
+                out.dtype in (np.float32, np.float64) and out.shape[0] >= self.M and
+                out.shape[1] >= self.M):
+            raise ValueError("out must be a C-contiguous float32/float64 M x M array")
+        ei, ej = ctypes.c_int64(-1), ctypes.c_int64(-1)
+        _native.check(self._lib.pcf_collection_fill_block(
+            self._h, int(r0), int(r1), int(op), float(p), int(bool(apply_root)),
+            int(bool(diag)), float(a), float(b), 0 if exact else 6, _native.ptr(out),
+            int(out.dtype == np.float32), out.shape[1], ctypes.byref(ei), ctypes.byref(ej)),
+            "pcf_collection_fill_block")
+        return None if ei.value < 0 else (int(ei.value), int(ej.value))
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h is not None and getattr(self, "_lib", None) is not None:
+            self._lib.pcf_collection_free(h)
 
 
 _CUDA = _Backend()

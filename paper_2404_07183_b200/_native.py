@@ -98,6 +98,11 @@ SIGNATURES = {
     "pcf_jit_single": (
         c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, c_vp, c_vp, c_vp]),
     "pcf_probe_fp64": (c_int, [c_vp, c_int, c_int, c_vp]),
+    "pcf_pow_batch": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "pcf_collection_create": (c_int, [c_vp, c_vp, c_int, c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    "pcf_collection_free": (None, [c_vp]),
+    "pcf_collection_fill_block": (c_int, [c_vp, c_i64, c_i64, c_int, c_dbl, c_int, c_int, c_dbl,
+                                          c_dbl, c_i32, c_vp, c_int, c_i64, c_i64p, c_i64p]),
     "pcf_scan_workspace": (c_int, [c_i64, c_i64p]),
     "pcf_compact": (
         c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64,

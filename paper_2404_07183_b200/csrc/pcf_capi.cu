@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <vector>
 #include "pcf_internal.h"
+#include "pcf_pow.cuh"
 
 namespace pcfb {
 
@@ -381,7 +382,7 @@ int pcf_fill_matrix(const void* recs_dev, const void* recs8_dev, const int64_t* 
   if (n_items <= 0) return PCF_OK;
   if (!recs_dev || !soff_dev || !perm_dev || !items_dev || !counter_dev || !out_dev || !err_dev ||
       (smem_mode && (!recs8_dev || !goff8_dev)) ||
-      ld < M || (op != PCF_OP_LP && op != PCF_OP_INNER) || !(a >= 0.0) || !(a < b) ||
+      ld < M || !pcf_op_ok(op) || !(a >= 0.0) || !(a < b) ||
       n_items > 0x7fffffff) {
     set_error("pcf_fill_matrix: bad arguments");
     return PCF_ERR_ARG;
@@ -435,7 +436,7 @@ int pcf_fill_rows(const void* recs_dev, const int64_t* soff_dev, const int32_t* 
                   unsigned long long* err_dev, void* stream) {
   if (r1 <= r0) return PCF_OK;
   if (!recs_dev || !soff_dev || !inv_dev || !slab_dev || !err_dev || r0 < 0 || r1 > M ||
-      (op != PCF_OP_LP && op != PCF_OP_INNER)) {
+      !pcf_op_ok(op)) {
     set_error("pcf_fill_rows: bad arguments");
     return PCF_ERR_ARG;
   }
@@ -463,7 +464,7 @@ int pcf_pair_list(const void* recs_dev, const int64_t* soff_dev, const int64_t* 
                   int64_t npairs, int op, double p, double a, double b, double* res_dev,
                   void* stream) {
   if (npairs <= 0) return PCF_OK;
-  if (!recs_dev || !soff_dev || !pairs_dev || !res_dev || (op != PCF_OP_LP && op != PCF_OP_INNER)) {
+  if (!recs_dev || !soff_dev || !pairs_dev || !res_dev || !pcf_op_ok(op)) {
     set_error("pcf_pair_list: bad arguments");
     return PCF_ERR_ARG;
   }
@@ -486,38 +487,85 @@ struct DevBuf {
 int pcf_integrate_pair_host(const double* ft, const double* fv, int64_t nf, const double* gt,
                             const double* gv, int64_t ng, double a, double b, int op, double p,
                             double* result) {
-  if (!ft || !fv || !gt || !gv || !result || nf < 1 || ng < 1) {
+  if (!ft || !fv || !gt || !gv || !result || nf < 1 || ng < 1 || !pcf_op_ok(op)) {
     set_error("pcf_integrate_pair_host: bad arguments");
     return PCF_ERR_ARG;
   }
+  // One pinned staging block and one device block per host thread, reused across calls:
+  // [t: N][v: N][off: 3][perm: 2 x int32 + pad][pairs: 2] goes up in ONE copy, the pack
+  // and the pair kernel run on the thread's stream, 8 bytes come back.
+  struct PairWs {
+    char* host = nullptr;
+    char* dev = nullptr;
+    size_t cap = 0;
+    cudaStream_t st = nullptr;
+    int device = -1;
+    ~PairWs() {
+      if (host) cudaFreeHost(host);
+      if (dev) cudaFree(dev);
+      if (st) cudaStreamDestroy(st);
+    }
+  };
+  thread_local PairWs ws;
   const int64_t N = nf + ng;
-  std::vector<double> tc(N), vc(N);
-  std::copy(ft, ft + nf, tc.begin());
-  std::copy(gt, gt + ng, tc.begin() + nf);
-  std::copy(fv, fv + nf, vc.begin());
-  std::copy(gv, gv + ng, vc.begin() + nf);
-  int64_t off[3] = {0, nf, N};
-  int32_t perm[2] = {0, 1};
-  int64_t pairs[2] = {0, 1};
-  DevBuf dt, dv, doff, dperm, drec, dpairs, dres;
-  cudaError_t e;
-  if ((e = dt.alloc(N * 8)) || (e = dv.alloc(N * 8)) || (e = doff.alloc(24)) ||
-      (e = dperm.alloc(8)) || (e = drec.alloc(N * 16)) || (e = dpairs.alloc(16)) ||
-      (e = dres.alloc(8)))
-    return cuda_fail(e, "pcf_integrate_pair_host alloc");
-  cudaMemcpy(dt.p, tc.data(), N * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(dv.p, vc.data(), N * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(doff.p, off, 24, cudaMemcpyHostToDevice);
-  cudaMemcpy(dperm.p, perm, 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(dpairs.p, pairs, 16, cudaMemcpyHostToDevice);
-  if ((e = launch_pack(dt.p, dv.p, 0, (int64_t*)doff.p, (int32_t*)dperm.p, (int64_t*)doff.p, 2,
-                       drec.p, nullptr, nullptr, 0)))
-    return cuda_fail(e, "pcf_integrate_pair_host pack");
-  if ((e = launch_pair_list(drec.p, (int64_t*)doff.p, (int64_t*)dpairs.p, 1, op, p, a, b,
-                            (double*)dres.p, 0)))
-    return cuda_fail(e, "pcf_integrate_pair_host kernel");
-  if ((e = cudaMemcpy(result, dres.p, 8, cudaMemcpyDeviceToHost)))
-    return cuda_fail(e, "pcf_integrate_pair_host copy");
+  const size_t up = (size_t)N * 16 + 24 + 16 + 16;  // t, v, off, perm (padded), pairs
+  const size_t rec_at = (up + 15) & ~(size_t)15;       // 16-byte records
+  const size_t need = rec_at + (size_t)N * 16 + 8;     // + records + result
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return cuda_fail(e, "pcf_integrate_pair_host device");
+  if (ws.device != dev) {
+    if (ws.dev) cudaFree(ws.dev);
+    if (ws.st) cudaStreamDestroy(ws.st);
+    ws.dev = nullptr;
+    ws.st = nullptr;
+    ws.cap = 0;
+    ws.device = dev;
+  }
+  if (!ws.st && (e = cudaStreamCreateWithFlags(&ws.st, cudaStreamNonBlocking)))
+    return cuda_fail(e, "pcf_integrate_pair_host stream");
+  if (ws.cap < need) {
+    if (ws.host) cudaFreeHost(ws.host);
+    if (ws.dev) cudaFree(ws.dev);
+    ws.host = ws.dev = nullptr;
+    ws.cap = 0;
+    const size_t cap = std::max<size_t>(need, 1 << 16);
+    if ((e = cudaHostAlloc((void**)&ws.host, cap, cudaHostAllocDefault)) ||
+        (e = cudaMalloc((void**)&ws.dev, cap)))
+      return cuda_fail(e, "pcf_integrate_pair_host alloc");
+    ws.cap = cap;
+  }
+  double* ht = (double*)ws.host;
+  double* hv = ht + N;
+  int64_t* hoff = (int64_t*)(hv + N);
+  int32_t* hperm = (int32_t*)(hoff + 3);
+  int64_t* hpairs = (int64_t*)((char*)hperm + 16);
+  memcpy(ht, ft, nf * 8);
+  memcpy(ht + nf, gt, ng * 8);
+  memcpy(hv, fv, nf * 8);
+  memcpy(hv + nf, gv, ng * 8);
+  hoff[0] = 0;
+  hoff[1] = nf;
+  hoff[2] = N;
+  hperm[0] = 0;
+  hperm[1] = 1;
+  hpairs[0] = 0;
+  hpairs[1] = 1;
+  char* d = ws.dev;
+  const double* dt = (const double*)d;
+  const double* dv = dt + N;
+  const int64_t* doff = (const int64_t*)(dv + N);
+  const int32_t* dperm = (const int32_t*)(doff + 3);
+  const int64_t* dpairs = (const int64_t*)((const char*)dperm + 16);
+  void* drec = d + rec_at;
+  double* dres = (double*)(d + rec_at + (size_t)N * 16);
+  if ((e = cudaMemcpyAsync(d, ws.host, up, cudaMemcpyHostToDevice, ws.st)) ||
+      (e = launch_pack(dt, dv, 0, doff, dperm, doff, 2, drec, nullptr, nullptr, ws.st)) ||
+      (e = launch_pair_list(drec, doff, dpairs, 1, op, p, a, b, dres, ws.st)) ||
+      (e = cudaMemcpyAsync(ws.host, dres, 8, cudaMemcpyDeviceToHost, ws.st)) ||
+      (e = cudaStreamSynchronize(ws.st)))
+    return cuda_fail(e, "pcf_integrate_pair_host");
+  memcpy(result, ws.host, 8);
   return PCF_OK;
 }
 
@@ -624,6 +672,28 @@ __global__ void k_probe_dfma(double* out, int iters, double seed) {
   if (s == 12345.678) out[0] = s;  // keep the work alive
 }
 }  // namespace pcfb
+
+namespace pcfb {
+__global__ void k_pow_batch(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                            double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = pcfpow::pow(x[i], y[i]);
+}
+}  // namespace pcfb
+
+extern "C" int pcf_pow_batch(const double* x_dev, const double* y_dev, int64_t n,
+                             double* out_dev, void* stream) {
+  if (n < 0 || (n > 0 && (!x_dev || !y_dev || !out_dev))) {
+    set_error("pcf_pow_batch: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  if (n == 0) return PCF_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  pcfb::k_pow_batch<<<grid, 256, 0, (cudaStream_t)stream>>>(x_dev, y_dev, n, out_dev);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PCF_OK : cuda_fail(e, "pcf_pow_batch");
+}
 
 extern "C" int pcf_probe_fp64(double* out_dev, int iters, int blocks_per_sm, void* stream) {
   const int nsm = num_sms_current();

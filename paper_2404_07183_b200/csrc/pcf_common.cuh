@@ -22,6 +22,10 @@ typedef unsigned int uint32_t;
 #endif
 #endif
 
+#ifndef __CUDACC_RTC__
+#include "pcf_pow.cuh"  // libm-exact pow (glibc 2.39 restated; tables from libm.so.6)
+#endif
+
 namespace pcfb {
 
 struct __align__(16) Rec {
@@ -36,9 +40,12 @@ struct __align__(8) Rec32 {
   float v;
 };
 
-// Integrand kinds.  OP_LP with p=1/2/3 get exact-arithmetic specialisations; any
-// other p goes through pow().  OP_INNER is v_f * v_g.
-enum HKind { H_L1 = 0, H_L2 = 1, H_L3 = 2, H_LP = 3, H_INNER = 4, H_USER = 5 };
+// Integrand kinds.  OP_LP: p = 1 is |x - y| (pow(d, 1.0) == d exactly); any other p is
+// H_LPX = pow(|x - y|, p) with the C library's pow restated bit for bit (pcf_pow.cuh), as
+// the reference computes every cell (pyx:43-46).  PCF_OP_FAST_POW (fast plan) trades that
+// for d*d (H_L2), d*d*|d| (H_L3) or CUDA's pow (H_LP): within 1 ulp per cell, rel 1e-12
+// per entry.  OP_INNER is v_f * v_g.
+enum HKind { H_L1 = 0, H_L2 = 1, H_L3 = 2, H_LP = 3, H_INNER = 4, H_USER = 5, H_LPX = 6 };
 
 // A user integrand compiled at run time (pcf_jit.cu defines it; never referenced by the
 // nvcc-built kernels, where HK is one of the op codes above).
@@ -59,6 +66,9 @@ __device__ __forceinline__ double hval(double x, double y, double p) {
     return __dmul_rn(__dmul_rn(d, d), d);
   }
   if (HK == H_LP) return pow(fabs(__dsub_rn(x, y)), p);
+#ifndef __CUDACC_RTC__
+  if constexpr (HK == H_LPX) return pcfpow::pow(fabs(__dsub_rn(x, y)), p);
+#endif
   if constexpr (HK == H_USER) return pcf_user_h(x, y);
   return __dmul_rn(x, y);
 }
@@ -144,10 +154,15 @@ __device__ __forceinline__ int upper_bound_count(int n, double a, KeyF key) {
   return lo;
 }
 
+// fill_block's root pow(acc, 1/p) (pyx:98,113-114) with the C library's pow, bit for bit
+// (pow(x, 1.0) == x exactly, so p = 1 skips it)
 __device__ __forceinline__ double root_p(double acc, double p) {
   if (p == 1.0) return acc;
-  if (p == 2.0) return sqrt(acc);
+#ifndef __CUDACC_RTC__
+  return pcfpow::pow(acc, 1.0 / p);
+#else
   return pow(acc, 1.0 / p);
+#endif
 }
 
 template <typename T> __device__ __forceinline__ T cast_out(double x);

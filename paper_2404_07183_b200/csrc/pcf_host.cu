@@ -144,7 +144,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
                     int64_t* err_j, void* stream) {
   if (err_i) *err_i = -1;
   if (err_j) *err_j = -1;
-  if (!tcat || !vcat || !off || !out || M < 1 || ld < M || (op != PCF_OP_LP && op != PCF_OP_INNER) ||
+  if (!tcat || !vcat || !off || !out || M < 1 || ld < M || !pcf_op_ok(op) ||
       !(a >= 0.0) || !(a < b) || M > 0x7fffffff) {
     set_error("pcf_matrix_host: bad arguments");
     return PCF_ERR_ARG;

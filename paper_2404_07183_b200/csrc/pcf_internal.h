@@ -51,6 +51,10 @@ struct RowsArgs {
 };
 
 int hkind_of(int op, double p);
+inline bool pcf_op_ok(int op) {
+  const int base = op & ~PCF_OP_FAST_POW;
+  return base == PCF_OP_LP || base == PCF_OP_INNER;
+}
 cudaError_t launch_fill_tiles(const FillArgs& A, cudaStream_t st);
 cudaError_t launch_diag(const void* recs, const int64_t* soff, const int32_t* perm, int64_t M,
                         int gram, double a, double b, void* out, int out_f32, int64_t ld,

@@ -341,13 +341,15 @@ static cudaError_t dispatch_hk(int hk, const FillArgs& A, cudaStream_t st) {
     case H_L2: return launch_tiles<H_L2, BOUNDED, OutT>(A, st);
     case H_L3: return launch_tiles<H_L3, BOUNDED, OutT>(A, st);
     case H_LP: return launch_tiles<H_LP, BOUNDED, OutT>(A, st);
+    case H_LPX: return launch_tiles<H_LPX, BOUNDED, OutT>(A, st);
     default: return launch_tiles<H_INNER, BOUNDED, OutT>(A, st);
   }
 }
 
 int hkind_of(int op, double p) {
-  if (op == 1) return H_INNER;
+  if ((op & ~PCF_OP_FAST_POW) == PCF_OP_INNER) return H_INNER;
   if (p == 1.0) return H_L1;
+  if (!(op & PCF_OP_FAST_POW)) return H_LPX;  // the reference's libm pow, bit for bit
   if (p == 2.0) return H_L2;
   if (p == 3.0) return H_L3;
   return H_LP;
@@ -403,6 +405,7 @@ static void rows_hk(int hk, const RowsArgs& A, cudaStream_t st) {
     case H_L2: launch_rows_t<H_L2, BOUNDED, OutT>(A, st); break;
     case H_L3: launch_rows_t<H_L3, BOUNDED, OutT>(A, st); break;
     case H_LP: launch_rows_t<H_LP, BOUNDED, OutT>(A, st); break;
+    case H_LPX: launch_rows_t<H_LPX, BOUNDED, OutT>(A, st); break;
     default: launch_rows_t<H_INNER, BOUNDED, OutT>(A, st); break;
   }
 }
@@ -440,6 +443,7 @@ cudaError_t launch_pair_list(const void* recs, const int64_t* soff, const int64_
     case H_L2: PCF_PL(H_L2); break;
     case H_L3: PCF_PL(H_L3); break;
     case H_LP: PCF_PL(H_LP); break;
+    case H_LPX: PCF_PL(H_LPX); break;
     default: PCF_PL(H_INNER); break;
   }
 #undef PCF_PL

@@ -16,6 +16,13 @@ from .collection import DeviceCollection, current_stream_handle
 
 OP_LP = 0
 OP_INNER = 1
+# include/pcf_b200.h PCF_OP_FAST_POW: the fast plan may evaluate L_p cells (p != 1) with
+# d*d / d*d*|d| / CUDA pow; without it every cell uses the C library's pow bit for bit
+OP_FAST_POW = 0x10
+
+
+def op_code(op, exact):
+    return int(op) | (OP_FAST_POW if (not exact and int(op) == OP_LP) else 0)
 
 _NO_ERR = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -85,7 +92,8 @@ def fill_pairwise(coll: DeviceCollection, op, p, apply_root, diag, a=0.0, b=math
             _native.check(lib.pcf_fill_matrix(
                 _native.ptr(coll.tile_recs), _native.ptr(coll.recsg), _native.ptr(coll.soff),
                 _native.ptr(coll.goff), _native.ptr(coll.perm), M,
-                ptr_items, s1 - s0, smem, mode, coll.rec_bytes, _native.ptr(counter), int(op), float(p),
+                ptr_items, s1 - s0, smem, mode, coll.rec_bytes, _native.ptr(counter),
+                op_code(op, exact), float(p),
                 int(bool(apply_root)), float(a), float(b), _native.ptr(out), out_f32, ld,
                 _native.ptr(err), st), "pcf_fill_matrix")
             if between_chunks is not None:
@@ -227,7 +235,8 @@ def matrix_host(tcat, vcat, off, op, p, apply_root, diag, a=0.0, b=math.inf, exa
 
     ei, ej = ctypes.c_int64(-1), ctypes.c_int64(-1)
     _native.check(lib.pcf_matrix_host(
-        _native.ptr(tcat), _native.ptr(vcat), int(f32), _native.ptr(off), M, int(op), float(p),
+        _native.ptr(tcat), _native.ptr(vcat), int(f32), _native.ptr(off), M,
+        op_code(op, exact), float(p),
         int(bool(apply_root)), int(bool(diag)), float(a), float(b), 0 if exact else 6,
         int(n_chunks), _native.ptr(out), int(ld), ctypes.byref(ei), ctypes.byref(ej), stream),
         "pcf_matrix_host")

@@ -128,20 +128,28 @@ class MatrixJob:
         return self._cancel.is_set()
 
     def run(self, workers=None, device_output=False, exact=None):
-        """Compute the matrix.  exact=True sums every entry with one lane, strictly left
-        to right like the reference (bitwise for p=1 and the Gram matrix); the default
-        (env PCF_B200_EXACT unset) lets up to a warp share a long pair, which sums the
-        same cell products in a different order (relative error < 1e-13 for L_p)."""
+        """Compute the matrix.  Default (exact, env PCF_B200_EXACT unset or 1): every entry
+        is summed by one lane strictly left to right with the C library's pow, like the
+        reference -- bit-identical to it and to lp_distance / l2_inner_product for every
+        p (test_matrix.py:41-47,97-102).  exact=False (or PCF_B200_EXACT=0) lets up to a
+        warp share a long pair and evaluates p = 2, 3 cells as products: the same cells
+        summed in G runs, relative error < 1e-13.
+
+        A host result with no progress sinks goes through the whole-matrix host-buffer
+        call (pcf_matrix_host): upload, device pack, one persistent fill launch, and the
+        D2H of finished rows into a pinned result while later rows compute."""
         exact_arg = exact
         if exact is None:
-            exact = os.environ.get("PCF_B200_EXACT", "") not in ("", "0")
+            exact = os.environ.get("PCF_B200_EXACT", "1").strip() not in ("0", "false", "")
         resolve_workers(workers)
+        if self._cancel.is_set():
+            raise errors.Cancelled("matrix job cancelled; partial work discarded")
+        if (self._integral is None and not device_output and not self._sinks):
+            return self._run_host(bool(exact))
         from .collection import DeviceCollection
 
         coll = DeviceCollection.from_pcfs(self._coll)
         M = coll.M
-        if self._cancel.is_set():
-            raise errors.Cancelled("matrix job cancelled; partial work discarded")
         last = [0.0]
 
         def report(frac):
@@ -165,6 +173,26 @@ class MatrixJob:
         self.entries_computed = M * (M + 1) // 2 if self._diag else M * (M - 1) // 2
         data = out if device_output else out.cpu().numpy()
         return PairwiseMatrix(data, True, self.entries_computed)
+
+    def _run_host(self, exact):
+        """Host result through pcf_matrix_host (see run)."""
+        from .collection import require_cuda
+        from .datagen import pack_matrices
+        from .engine import matrix_host
+
+        torch = require_cuda()
+        tcat, vcat, off = pack_matrices([f.to_matrix() for f in self._coll], self._dtype)
+        M = int(off.shape[0] - 1)
+        # pinned (page-locked) result from torch's caching host allocator, so the row
+        # copies overlap the fill; the returned array keeps the buffer alive
+        tdt = torch.float32 if self._dtype == np.float32 else torch.float64
+        out = torch.empty((M, M), dtype=tdt, pin_memory=True).numpy()
+        out, bad = matrix_host(tcat, vcat, off, self._op, self._p, self._apply_root,
+                               self._diag, self._a, self._b, exact=exact, out=out)
+        if bad is not None:
+            raise self._divergence_error(bad)
+        self.entries_computed = M * (M + 1) // 2 if self._diag else M * (M - 1) // 2
+        return PairwiseMatrix(out, True, self.entries_computed)
 
     def _run_custom(self, coll, report, device_output, exact=None):
         """Arbitrary CombinationIntegral (matrix.py:184-196): the integrand is compiled

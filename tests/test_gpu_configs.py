@@ -134,6 +134,11 @@ def test_c4_heavy_tail_lp(p):
     worst = max(rel(D[i, i + 1:], ref[i][i + 1:]) for i in rows)
     assert worst < 1e-12, worst
     assert np.array_equal(D, D.T)
+    # exact plan: one lane per pair and the C library's pow on every cell and root --
+    # bit-identical to the reference for p = 2, 3 as well
+    D = fill(coll, 0, p, True, False, exact=True).cpu().numpy()
+    for i in rows:
+        assert np.array_equal(D[i, i + 1:], ref[i][i + 1:]), i
 
 
 def test_c3_rows_exact_bitwise_and_fast():
