@@ -42,10 +42,32 @@ __device__ __forceinline__ double pcf_npmax(double a, double b) {
 __device__ __forceinline__ double pcf_npmin(double a, double b) {
   return (a != a || b != b) ? PCF_NAN : (b < a ? b : a);
 }
+// CPython float % and // (Objects/floatobject.c float_rem / float_floor_div): the
+// remainder takes the divisor's sign (a zero remainder is copysign(0, y)), the quotient is
+// (x - mod) / y snapped to the nearest integer, not floor(x / y): 1.0 // 0.1 == 9.0
 __device__ __forceinline__ double pcf_pymod(double x, double y) {
   double r = fmod(x, y);
-  if (r != 0.0 && ((r < 0.0) != (y < 0.0))) r += y;
+  if (r != 0.0) {
+    if ((y < 0.0) != (r < 0.0)) r = __dadd_rn(r, y);
+  } else {
+    r = copysign(0.0, y);
+  }
   return r;
+}
+__device__ __forceinline__ double pcf_pyfloordiv(double x, double y) {
+  double mod = fmod(x, y);
+  double div = __ddiv_rn(__dsub_rn(x, mod), y);
+  if (mod != 0.0) {
+    if ((y < 0.0) != (mod < 0.0)) div = __dsub_rn(div, 1.0);
+  }
+  double fd;
+  if (div != 0.0) {
+    fd = floor(div);
+    if (__dsub_rn(div, fd) > 0.5) fd = __dadd_rn(fd, 1.0);
+  } else {
+    fd = copysign(0.0, __ddiv_rn(x, y));
+  }
+  return fd;
 }
 __device__ __forceinline__ double pcf_sq(double x) { return __dmul_rn(x, x); }
 

@@ -124,7 +124,7 @@ class _Translator:
             if op is ast.Mod:
                 return f"pcf_pymod({a}, {b})"
             if op is ast.FloorDiv:
-                return f"floor({a} / {b})"
+                return f"pcf_pyfloordiv({a}, {b})"
             if op is ast.Pow:
                 if isinstance(node.right, ast.Constant) and node.right.value == 2:
                     return f"pcf_sq({a})"
@@ -349,8 +349,8 @@ class _Sym:
     def __rtruediv__(self, o): return self._bin(o, "({} / {})", True)
     def __mod__(self, o): return self._bin(o, "pcf_pymod({}, {})")
     def __rmod__(self, o): return self._bin(o, "pcf_pymod({}, {})", True)
-    def __floordiv__(self, o): return self._bin(o, "floor({} / {})")
-    def __rfloordiv__(self, o): return self._bin(o, "floor({} / {})", True)
+    def __floordiv__(self, o): return self._bin(o, "pcf_pyfloordiv({}, {})")
+    def __rfloordiv__(self, o): return self._bin(o, "pcf_pyfloordiv({}, {})", True)
 
     def __pow__(self, o):
         if isinstance(o, (int, float)) and o == 2:
@@ -434,6 +434,7 @@ def generate(h=None, H=None, r=None, u=None):
             "__device__ __forceinline__ double pcf_npmax(double a, double b);\n"
             "__device__ __forceinline__ double pcf_npmin(double a, double b);\n"
             "__device__ __forceinline__ double pcf_pymod(double x, double y);\n"
+            "__device__ __forceinline__ double pcf_pyfloordiv(double x, double y);\n"
             "__device__ __forceinline__ double pcf_sq(double x);\n")
     return head + unit.source(entries)
 

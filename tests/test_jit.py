@@ -40,7 +40,7 @@ K = 3.0
 def test_semantics_of_translation():
     src = jit.generate(h=lambda x, y: max(x, y, K) % 2 if not x else -y // 4)
     assert "pcf_pymax(pcf_pymax(a_x, a_y), (0x1.8000000000000p+1))" in src
-    assert "pcf_pymod" in src and "floor(" in src
+    assert "pcf_pymod" in src and "pcf_pyfloordiv(" in src
     src = jit.generate(h=lambda x, y: (x - y) ** 2 + math.pi)
     assert "pcf_sq((a_x - a_y))" in src and float.hex(math.pi) in src
 
