@@ -86,25 +86,21 @@ cudaError_t copy_rows(const std::vector<int32_t>& perm, const std::vector<int32_
   const size_t n = rows.size();
   static const bool no_d2h = getenv("PCF_HOST_NO_D2H") != nullptr;  // timing experiments
   if (n == 0 || no_d2h) return cudaSuccess;
-  std::vector<void*> dst(n), src(n);
-  std::vector<size_t> sizes(n, (size_t)M * es);
-  for (size_t k = 0; k < n; ++k) {
-    const int64_t o = perm[rows[k]];
-    src[k] = (void*)(dsrc + (size_t)o * (size_t)M * es);
-    dst[k] = (void*)(hdst + (size_t)o * (size_t)ld * es);
-  }
-  cudaMemcpyAttributes attr;
-  memset(&attr, 0, sizeof(attr));
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t attr_idx = 0, fail_idx = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), n, &attr, &attr_idx,
-                                       1, &fail_idx, st);
-  if (e == cudaSuccess) return e;
-  cudaGetLastError();  // batch API unavailable (old driver): one copy per row
-  for (size_t k = 0; k < n; ++k) {
-    e = cudaMemcpyAsync(dst[k], src[k], sizes[k], cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return e;
+  // original row indices in ascending order, coalesced into runs of consecutive rows:
+  // one pitched copy per run (source pitch M, host pitch ld)
+  std::vector<int64_t> o(n);
+  for (size_t k = 0; k < n; ++k) o[k] = perm[rows[k]];
+  std::sort(o.begin(), o.end());
+  const size_t row_bytes = (size_t)M * es;
+  for (size_t k = 0; k < n;) {
+    size_t e = k + 1;
+    while (e < n && o[e] == o[e - 1] + 1) ++e;
+    const cudaError_t rc = cudaMemcpy2DAsync(
+        hdst + (size_t)o[k] * (size_t)ld * es, (size_t)ld * es,
+        dsrc + (size_t)o[k] * row_bytes, row_bytes, row_bytes, e - k,
+        cudaMemcpyDeviceToHost, st);
+    if (rc != cudaSuccess) return rc;
+    k = e;
   }
   return cudaSuccess;
 }
