@@ -40,6 +40,9 @@ METRIC = "PCF pair-integrals/sec (100k-PCF L1 distance matrix)"
 BACKEND = os.environ.get("PCF_BENCH_BACKEND", "nccl")
 UNIT = "pair-integrals/s"
 FLOPS_PER_CELL_L1 = 4  # |vf - vg|, tn - t, mul, add
+# planner smem_mode -> kernel (csrc/pcf_tiles.cuh)
+KERNEL_NAMES = {1: "k_fill_tiles_smem", 3: "k_fill_colgroups", 4: "k_fill_rows_staged",
+                2: "k_fill_rowres", 0: "k_fill_tiles_global"}
 
 
 def parse():
@@ -51,6 +54,8 @@ def parse():
     ap.add_argument("--M", type=int, default=100000)
     ap.add_argument("--exact", action="store_true", help="one lane per pair (bitwise mode)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other", action="store_true",
+                    help="skip the second (exact when the headline is fast) device timing")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -292,71 +297,89 @@ def run_ours(args):
     t, v, off, pairs, cells = workload(M)
 
     coll = DeviceCollection(t, v, off, device=dev)
-    _, host_items, smem = coll.plan(exact=args.exact)
-    my_items = partition_items(host_items, world, rank)
-    items_dev = items_to_device(my_items, dev)
-    my_cells = item_cells(my_items, coll.sizes_sorted)
     out = torch.empty((M, M), dtype=torch.float64, device=dev)
     err = new_err(dev)
     counter = torch.zeros(1, dtype=torch.int32, device=dev)
     st = current_stream_handle()
     stream = torch.cuda.current_stream()
 
-    ev_k = []
+    def timed_fill(exact, steps, warmup, sample_clocks):
+        """Plan (exact or fast), then `warmup` untimed and `steps` timed whole-matrix
+        fills bracketed by barrier + synchronize; returns the max-over-ranks time, the
+        per-kernel-mode CUDA-event averages (each launch timed on the stream it runs on)
+        and the cells each mode covers."""
+        _, host_items, smem = coll.plan(exact=exact)
+        my_items = partition_items(host_items, world, rank)
+        items_dev = items_to_device(my_items, dev)
+        runs = mode_runs(my_items)
+        ev = {mode: [] for _, _, mode in runs}
 
-    def step(record=False):
-        launches = 0
-        if rank == 0:  # one writer per entry across ranks: the diagonal is rank 0's
-            lib.pcf_fill_diagonal(_native.ptr(coll.recs), _native.ptr(coll.soff),
-                                  _native.ptr(coll.perm), M, 0, 0.0, math.inf,
-                                  _native.ptr(out), 0, M, _native.ptr(err), st)
-            launches = 1
-        for lo, hi, mode in mode_runs(my_items):
-            cnt = hi - lo
-            if record and mode == 1:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-            rc = lib.pcf_fill_matrix(
-                _native.ptr(coll.tile_recs), _native.ptr(coll.recsg), _native.ptr(coll.soff),
-                _native.ptr(coll.goff), _native.ptr(coll.perm), M,
-                _native.c_vp(items_dev.data_ptr() + lo * 32), cnt, smem, mode, coll.rec_bytes,
-                _native.ptr(counter), 0, 1.0, 1, 0.0, math.inf, _native.ptr(out), 0, M,
-                _native.ptr(err), st)
-            _native.check(rc, "pcf_fill_matrix")
-            launches += 1
-            if record and mode == 1:
-                b.record(stream)
-                ev_k.append((a, b))
-        return launches
+        def step(record=False):
+            launches = 0
+            if rank == 0:  # one writer per entry across ranks: the diagonal is rank 0's
+                lib.pcf_fill_diagonal(_native.ptr(coll.recs), _native.ptr(coll.soff),
+                                      _native.ptr(coll.perm), M, 0, 0.0, math.inf,
+                                      _native.ptr(out), 0, M, _native.ptr(err), st)
+                launches = 1
+            for lo, hi, mode in runs:
+                if record:
+                    a, b = (torch.cuda.Event(enable_timing=True),
+                            torch.cuda.Event(enable_timing=True))
+                    a.record(stream)
+                rc = lib.pcf_fill_matrix(
+                    _native.ptr(coll.tile_recs), _native.ptr(coll.recsg),
+                    _native.ptr(coll.soff), _native.ptr(coll.goff), _native.ptr(coll.perm), M,
+                    _native.c_vp(items_dev.data_ptr() + lo * 32), hi - lo, smem, mode,
+                    coll.rec_bytes, _native.ptr(counter), 0, 1.0, 1, 0.0, math.inf,
+                    _native.ptr(out), 0, M, _native.ptr(err), st)
+                _native.check(rc, "pcf_fill_matrix")
+                launches += 1
+                if record:
+                    b.record(stream)
+                    ev[mode].append((a, b))
+            return launches
 
-    for _ in range(max(args.warmup, 0)):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        tdist.barrier()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        for _ in range(args.steps):
-            launches += step(record=True)
-        t1.record(stream)
+        for _ in range(max(warmup, 0)):
+            step()
         torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev if BACKEND == "nccl" else "cpu")
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        tdist.barrier()
-        ms = float(tt.item())
-    bad = decode_err(err, M)
-    if bad is not None:
-        raise RuntimeError(f"non-finite entry {bad}")
-    value = pairs * args.steps / (ms * 1e-3)
-    kms = [a.elapsed_time(b) for a, b in ev_k]
-    k_avg = float(np.mean(kms)) if kms else float("nan")
-    smem_cells = item_cells(my_items[my_items[:, 6] == 1], coll.sizes_sorted)
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches = 0
+        with ClockSampler(local) as clk:
+            t0.record(stream)
+            for _ in range(steps):
+                launches += step(record=True)
+            t1.record(stream)
+            torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            tt = torch.tensor([ms], dtype=torch.float64,
+                              device=dev if BACKEND == "nccl" else "cpu")
+            tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+            tdist.barrier()
+            ms = float(tt.item())
+        bad = decode_err(err, M)
+        if bad is not None:
+            raise RuntimeError(f"non-finite entry {bad}")
+        kms = {mode: float(np.mean([a.elapsed_time(b) for a, b in e])) for mode, e in ev.items()}
+        mcells = {mode: item_cells(my_items[my_items[:, 6] == mode], coll.sizes_sorted)
+                  for mode in kms}
+        return {"ms": ms, "launches": launches, "kms": kms, "mcells": mcells,
+                "items": int(host_items.shape[0]), "smem": smem, "clk": clk}
+
+    def dominant(res):
+        """The kernel mode with the largest share of the step, its name, time and cells."""
+        mode = max(res["kms"], key=lambda m: res["kms"][m])
+        return mode, KERNEL_NAMES.get(mode, str(mode)), res["kms"][mode], res["mcells"][mode]
+
     peak = fp64_peak_tflops(lib, torch, st)
+    main = timed_fill(args.exact, args.steps, args.warmup, True)
+    ms = main["ms"]
+    clk = main["clk"]
+    value = pairs * args.steps / (ms * 1e-3)
+    dmode, dname, k_avg, smem_cells = dominant(main)
     achieved = FLOPS_PER_CELL_L1 * smem_cells / (k_avg * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
@@ -367,11 +390,34 @@ def run_ours(args):
                 traffic = tr.get("bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
+    launches = main["launches"]
+    host_items_n, smem = main["items"], main["smem"]
+    # the other mode (exact when the headline is fast), measured the same way on the same
+    # buffers: exact = one lane per pair summed left to right, bitwise equal to the
+    # reference kernel; it is what pdist()/l2_kernel() run by default
+    other = None
+    if not args.no_other:
+        o_steps = max(1, min(args.steps, 2))
+        o = timed_fill(not args.exact, o_steps, 1, False)
+        om, oname, oms, ocells = dominant(o)
+        other = {"mode": "fast (merge-path G lanes/pair)" if args.exact
+                 else "exact (1 lane/pair, bitwise vs the reference kernel)",
+                 "value": pairs * o_steps / (o["ms"] * 1e-3), "unit": UNIT,
+                 "ms_per_step": o["ms"] / o_steps, "steps": o_steps, "warmup": 1,
+                 "gpu_launches": o["launches"], "work_items": o["items"],
+                 "clocks": o["clk"].summary(),
+                 "dominant_kernel": {"name": oname, "kernel_ms": oms, "cells": ocells,
+                                     "cells_per_s_per_gpu": ocells / (oms * 1e-3),
+                                     "fp64_frac": FLOPS_PER_CELL_L1 * ocells
+                                     / (oms * 1e-3) / 1e12 / peak},
+                 "kernel_ms_by_mode": {KERNEL_NAMES.get(k, str(k)): v
+                                       for k, v in o["kms"].items()}}
+    del out
 
     # ---- end-to-end through the host-buffer path
     e2e = None
     if not args.no_e2e:
-        del out, coll, items_dev  # the e2e path holds its own 80 GB result buffer
+        del coll  # the e2e path holds its own 80 GB result buffer
         torch.cuda.empty_cache()
         e2e = run_e2e(args, t, v, off, pairs, world, rank, dev)
         lib.pcf_release_workspace()
@@ -399,17 +445,19 @@ def run_ours(args):
                 "parallelism": f"tile-queue split over {world} GPU(s)",
                 "l2": f"no flush needed: {16 * int(off[-1]) / 1e9:.2f} GB input records + "
                       f"{8 * M * M / 1e9:.1f} GB output per step >> 126 MB L2",
-                "work_items": int(host_items.shape[0]), "smem_bytes": smem,
+                "work_items": host_items_n, "smem_bytes": smem,
             },
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "roofline": {
-                "bound": "fp64", "kernel": "k_fill_tiles_smem",
+                "bound": "fp64", "kernel": dname,
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "peak_source": "measured live: DFMA probe (pcf_probe_fp64); MEASURED_PEAKS.json "
                                "has no FP64 figure",
                 "algorithmic": f"{FLOPS_PER_CELL_L1} flop/cell x {smem_cells:.4e} cells per launch",
+                "kernel_ms_by_mode": {KERNEL_NAMES.get(k, str(k)): v
+                                      for k, v in main["kms"].items()},
                 "kernel_ms": k_avg,
                 "cells_per_s_per_gpu": smem_cells / (k_avg * 1e-3),
                 "traffic_note": "ncu dram read+write per launch (profiles/k1_traffic.json); "
@@ -420,6 +468,7 @@ def run_ours(args):
                 "limiter": smem_limiter(smem_cells / (k_avg * 1e-3), clk.summary()),
             },
             "e2e": e2e,
+            "exact" if not args.exact else "fast": other,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -127,6 +127,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       getenv("PCF_SINGLE_FALLBACK_LOG2G") ? atoi(getenv("PCF_SINGLE_FALLBACK_LOG2G")) : -1;
   std::vector<pcf_work_item> runs[5];  // by kernel: K1 (mode 1), K1c (3), K1s (4), K1r (2), K1g (0)
   int64_t need_max = 0, k1r_need = 0, k1c_need = 0, k1s_need = 0;
+  const int64_t k1s_ring = (int64_t)kK1sRingSlots * kTileThreads * RB;  // K1s prefetch rings
   const int64_t n_groups = (M + GW - 1) / GW;
   // K1c (one long row resident, interleaved column groups streamed): the best config for a
   // column range starting at group ks -- largest CG (fewest segments) that fits, double
@@ -270,12 +271,13 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       logC = 9 - logG;
       k1r_need = std::max(k1r_need, al(sizes[r0] * RB));
     } else if (max_log2G == 0 && kK1sEnabled && (r0 % GW) == 0 &&
-               al(group_recs(r0) * RB) <= smem_budget) {
-      // K1s (exact mode): the row block staged as in K1, columns through L1, 64 quarters
-      // = RG x C columns per pass
+               al(group_recs(r0) * RB) + k1s_ring <= smem_budget) {
+      // K1s (exact mode): the row block staged as in K1, columns through each lane's
+      // prefetch ring, 64 quarters = RG x C columns per pass
       int64_t rows_b = group_recs(r0) * RB;
       int lrg = 0;
-      if (r0 + GW < M - 1 && al(rows_b + group_recs(r0 + GW) * RB) <= smem_budget) {
+      if (r0 + GW < M - 1 &&
+          al(rows_b + group_recs(r0 + GW) * RB) + k1s_ring <= smem_budget) {
         rows_b += group_recs(r0 + GW) * RB;
         lrg = 1;
       }
@@ -283,7 +285,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       logG = 0;
       logC = LOGU - lrg;
       s_mode = 4;
-      k1s_need = std::max(k1s_need, al(rows_b));
+      k1s_need = std::max(k1s_need, al(rows_b) + k1s_ring);
     } else {  // rows too long for shared memory: operands from L1/L2 (K1g)
       logG = std::min(max_log2G, 5);
       const int P = T >> logG;

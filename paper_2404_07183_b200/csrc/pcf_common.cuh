@@ -142,6 +142,41 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// ------------------------------------------------- per-thread async copies (LDGSTS)
+// One record global -> shared, completion tracked by the issuing thread's commit groups.
+// 16-byte records bypass L1 (.cg); 8-byte records must use .ca.
+template <int BYTES>
+__device__ __forceinline__ void cp_async_rec(uint32_t dst, const void* src) {
+  if constexpr (BYTES == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  }
+}
+
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// one record from a 32-bit shared-memory address
+__device__ __forceinline__ void lds_rec(uint32_t a, double& t, double& v) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(t), "=d"(v) : "r"(a));
+}
+__device__ __forceinline__ void lds_rec(uint32_t a, float& t, float& v) {
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(t), "=f"(v) : "r"(a));
+}
+
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+  uint32_t n;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(n));
+  return n;
+}
+
 // Largest count of x in [0, n) with key(x) <= a, for sorted keys (upper_bound).
 template <typename KeyF>
 __device__ __forceinline__ int upper_bound_count(int n, double a, KeyF key) {

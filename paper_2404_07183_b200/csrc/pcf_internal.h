@@ -7,6 +7,9 @@
 namespace pcfb {
 
 constexpr int kTileThreads = 512;  // CTA size of the persistent tile kernels
+// K1s column prefetch ring: slots per lane (pcf_tiles.cuh kRingSlots); the ring takes
+// kRingSlots * kTileThreads records at the top of the dynamic shared memory
+constexpr int kK1sRingSlots = 8;
 
 typedef pcf_work_item PcfWorkItem;
 

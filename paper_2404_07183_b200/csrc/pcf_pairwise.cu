@@ -10,6 +10,7 @@
 #include "pcf_common.cuh"
 #include "pcf_internal.h"
 #include "pcf_tiles.cuh"
+static_assert(pcfb::kRingSlots == pcfb::kK1sRingSlots, "K1s ring depth: planner and kernel disagree");
 
 namespace pcfb {
 

@@ -502,10 +502,117 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // --------------------------------------------------------------------------------------
 // K1s: exact mode (G = 1) for row blocks whose 64 columns per chunk do not fit next to
 // them.  The row block is staged as in K1 (interleaved groups, one bulk copy); the
-// columns are read straight from global memory through L1.  Lanes as in K1: a
-// quarter-warp is the GW rows of a group against ONE column, so the 8 lanes of a quarter
-// read nearby records of the same column (few L1 lines per request) and conflict-free
-// rows.  64 quarters = RG x C columns per pass; no per-pass barrier (nothing streamed).
+// columns stay in global memory and reach each lane through a private prefetch ring in
+// shared memory (kRingSlots records per lane, filled by per-thread cp.async = LDGSTS).
+//
+// Bank mapping: lane `tid` holds row slot u = tid % GW, whose records sit in bank group u
+// of the interleaved row block; its ring slot k sits at ring + (k * 512 + tid) records,
+// i.e. in bank group tid % GW as well.  Every shared load of a lane -- row or column --
+// hits its own bank group, so a quarter-warp is ONE wavefront whatever positions its
+// lanes are at (K1's shared column chunk pays ~2x in conflicts for that).
+//
+// Latency: when a lane's column cursor advances to record j it reads slot j % D and
+// refills the slot of record j - 1 (read at its previous column advance) with record
+// j + D - 1.  Record j + 1 was therefore requested >= D - 1 walk steps earlier; one commit
+// group per step, so cp.async.wait_group(D - 2) before the load guarantees it landed while
+// the last D - 2 steps' requests stay in flight (~L2 latency hidden behind D - 2 steps).
+constexpr int kRingSlots = 8;
+
+template <int HK, bool BOUNDED, typename RT>
+__device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int nf,
+                                                 const RT* __restrict__ gcol, int ng,
+                                                 uint32_t ring, double p, double a, double b) {
+  using ST = decltype(RT::t);
+  constexpr int D = kRingSlots;
+  constexpr uint32_t RB = (uint32_t)sizeof(RT);
+  constexpr uint32_t RS = 128;                 // row record stride (GW interleaved records)
+  constexpr uint32_t CS = kTileThreads * RB;   // ring slot stride
+  const int SF = 128 / (int)sizeof(RT);
+  int k0 = 0, m0 = 0;
+  if (a > 0.0) {  // start cursors k = max{i : t_i <= a} (pyx:33-36)
+    k0 = upper_bound_count(nf - 1, a, [&](int x) { return (double)F[x * SF].t; });
+    m0 = upper_bound_count(ng - 1, a, [&](int x) { return (double)gcol[x].t; });
+  }
+  const int steps = (nf - 1 - k0) + (ng - 1 - m0);
+  const char* gb = reinterpret_cast<const char*>(gcol);
+  // the previous pair's in-flight prefetches must land before their slots are reused
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const uint32_t r = (uint32_t)min(m0 + i, ng - 1);
+    cp_async_rec<sizeof(RT)>(ring + (uint32_t)((m0 + i) & (D - 1)) * CS, gb + r * RB);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  // column cursor j: its record sits in ring slot j % D; advancing to j + 1 frees slot
+  // j % D, which takes record j + D (clamped to the last record: never read)
+  int jc = m0;
+  const uint32_t cprev = ring + (uint32_t)(m0 & (D - 1)) * CS;
+  uint32_t rnext = smem_u32(F + k0 * SF);
+  ST tr, vr, tc, vc;
+  lds_rec(rnext, tr, vr);
+  lds_rec(cprev, tc, vc);
+  rnext += RS;
+  // X/Y walk (see lane_walk) with the column cursor's identity carried in xc: X is the
+  // cursor whose piece ends first; when the roles swap, X becomes the other cursor.
+  bool xc = tc < tr;
+  ST tx = xc ? tc : tr, ty = xc ? tr : tc, vy = xc ? vr : vc;
+  const ST vx = xc ? vc : vr;
+  double t = a;
+  if (BOUNDED) t = fmin(t, b);
+  double acc = 0.0;
+  double hc = hval<HK>((double)vx, (double)vy, p);
+  auto step = [&]() {
+    double tn = (double)tx;
+    if (BOUNDED) tn = fmin(tn, b);
+    if constexpr (HK == H_USER) {
+      const double dt = __dsub_rn(tn, t);
+      acc = __dadd_rn(acc, __dmul_rn(dt > 0.0 ? hc : 0.0, dt));
+    } else {
+      acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(tn, t)));
+    }
+    t = tn;
+    // slot addresses recomputed from jc each step (no loop-carried register is read by
+    // the in-flight LDGSTS, so nothing waits for the MIO queue to release it)
+    const uint32_t slot_cur = ring + (uint32_t)(jc & (D - 1)) * CS;
+    const uint32_t slot_nxt = ring + (uint32_t)((jc + 1) & (D - 1)) * CS;
+    const uint32_t addr = xc ? slot_nxt : rnext;
+    if (xc) {  // the column advances: refill the slot it leaves with record jc + D
+      const uint32_t r = (uint32_t)min(jc + D, ng - 1);
+      cp_async_rec<sizeof(RT)>(slot_cur, gb + r * RB);
+      ++jc;
+    } else {
+      rnext += RS;
+    }
+    ST nt, nv;
+    lds_rec(addr, nt, nv);
+    hc = hval<HK>((double)nv, (double)vy, p);
+    const bool sw = nt > ty;
+    tx = sw ? ty : nt;
+    ty = sw ? nt : ty;
+    vy = sw ? nv : vy;
+    xc = xc != sw;
+  };
+  // one commit group per two steps: a record read at step s was requested at step
+  // <= s - (D - 1), i.e. in a group at least 3 groups old, so waiting until <= 2 groups
+  // are pending before each pair of steps covers both
+  int s = 0;
+#pragma unroll 2
+  for (; s + 1 < steps; s += 2) {
+    cp_async_wait<(D - 3) / 2>();
+    step();
+    step();
+    cp_async_commit();
+  }
+  if (s < steps) {
+    cp_async_wait<(D - 3) / 2>();
+    step();
+    cp_async_commit();
+  }
+  if (BOUNDED && (HK != H_USER || b > t)) acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(b, t)));
+  return acc;
+}
+
 template <int HK, bool BOUNDED, typename OutT, typename RT, int GW>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_fill_rows_staged(const RT* __restrict__ recs, const RT* __restrict__ recsg,
@@ -520,6 +627,10 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   __shared__ uint64_t bar;
   __shared__ int s_item;
   const int tid = threadIdx.x;
+  // the lane's prefetch ring at the top of the dynamic shared memory (slot 0 address)
+  const uint32_t ring = smem_u32(smem) + dynamic_smem_bytes() -
+                        (uint32_t)(kRingSlots * kTileThreads * sizeof(RT)) +
+                        (uint32_t)(tid * sizeof(RT));
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -563,12 +674,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (row_ok && qs < W.col1 && qs > ps) {
         const RT* Gv = recs + soff[qs];
         const int ng = (int)(soff[qs + 1] - soff[qs]);
-        const double acc = lane_walk<HK, BOUNDED, GW, 1, RT>(F, nf, Gv, ng, 0, 0, p, a, b);
+        const double acc = lane_walk_ring<HK, BOUNDED, RT>(F, nf, Gv, ng, ring, p, a, b);
         const double hl = BOUNDED ? 0.0 : hval<HK>((double)F[(nf - 1) * GW].v,
                                                    (double)Gv[ng - 1].v, p);
         finish_entry<HK, BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
       }
     }
+    cp_async_wait<0>();  // no prefetch may land in the ring after the kernel moves on
     __syncthreads();  // every lane done with the rows before the next item's copy
     if (tag_done && tid == 0) signal_item(item_tag, tag_done, it);
   }
