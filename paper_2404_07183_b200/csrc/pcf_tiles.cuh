@@ -505,18 +505,21 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // columns stay in global memory and reach each lane through a private prefetch ring in
 // shared memory (kRingSlots records per lane, filled by per-thread cp.async = LDGSTS).
 //
-// Bank mapping: lane `tid` holds row slot u = tid % GW, whose records sit in bank group u
-// of the interleaved row block; its ring slot k sits at ring + (k * 512 + tid) records,
-// i.e. in bank group tid % GW as well.  Every shared load of a lane -- row or column --
-// hits its own bank group, so a quarter-warp is ONE wavefront whatever positions its
-// lanes are at (K1's shared column chunk pays ~2x in conflicts for that).
+// Bank mapping: lane L holds row slot u = L % GW, whose records sit in bank group u of
+// the interleaved row block.  Its ring slot k sits at
+//   ring_base + (L / GW) * (kRingSlots * 128) + k * 128 + (L % GW) * sizeof(RT)
+// -- bank group L % GW as well, for every k.  Every shared load of a lane (row record or
+// ring slot) hits its own bank group, so a quarter-warp is ONE wavefront whatever
+// positions its lanes are at (K1's shared column chunk pays ~2x in conflicts for that).
+// The ring base is 1 KB aligned, so the next slot is one add and one LOP3 (bits 7-9 wrap).
 //
-// Latency: when a lane's column cursor advances to record j it reads slot j % D and
-// refills the slot of record j - 1 (read at its previous column advance) with record
-// j + D - 1.  Record j + 1 was therefore requested >= D - 1 walk steps earlier; one commit
-// group per step, so cp.async.wait_group(D - 2) before the load guarantees it landed while
-// the last D - 2 steps' requests stay in flight (~L2 latency hidden behind D - 2 steps).
+// Latency: when a lane's column cursor advances it reads the next slot and refills the
+// slot it leaves with the record kRingSlots ahead.  A record is therefore requested
+// >= D - 1 walk steps before it is read; with one commit group per two steps,
+// cp.async.wait_group((D - 3) / 2) before each pair of steps guarantees it landed while
+// the last steps' requests stay in flight (~L2 latency hidden).
 constexpr int kRingSlots = 8;
+constexpr uint32_t kRingAlign = 1024;
 
 template <int HK, bool BOUNDED, typename RT>
 __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int nf,
@@ -525,8 +528,10 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
   using ST = decltype(RT::t);
   constexpr int D = kRingSlots;
   constexpr uint32_t RB = (uint32_t)sizeof(RT);
-  constexpr uint32_t RS = 128;                 // row record stride (GW interleaved records)
-  constexpr uint32_t CS = kTileThreads * RB;   // ring slot stride
+  constexpr uint32_t RS = 128;               // row record stride (GW interleaved records)
+  constexpr uint32_t CS = 128;               // ring slot stride
+  constexpr uint32_t WRAP = (D - 1) * CS;    // slot-index bits of a ring address
+  static_assert(D * CS <= kRingAlign && (D & (D - 1)) == 0, "ring slots");
   const int SF = 128 / (int)sizeof(RT);
   int k0 = 0, m0 = 0;
   if (a > 0.0) {  // start cursors k = max{i : t_i <= a} (pyx:33-36)
@@ -535,6 +540,7 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
   }
   const int steps = (nf - 1 - k0) + (ng - 1 - m0);
   const char* gb = reinterpret_cast<const char*>(gcol);
+  const uint32_t boff_last = (uint32_t)(ng - 1) * RB;
   // the previous pair's in-flight prefetches must land before their slots are reused
   cp_async_wait<0>();
 #pragma unroll
@@ -544,14 +550,17 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
   }
   cp_async_commit();
   cp_async_wait<0>();
-  // column cursor j: its record sits in ring slot j % D; advancing to j + 1 frees slot
-  // j % D, which takes record j + D (clamped to the last record: never read)
-  int jc = m0;
-  const uint32_t cprev = ring + (uint32_t)(m0 & (D - 1)) * CS;
+  uint32_t boff = (uint32_t)min(m0 + D, ng - 1) * RB;      // next record to request
+  const uint32_t cslot = ring + (uint32_t)(m0 & (D - 1)) * CS;  // the current column record
+  // loop-carried: the slot of the NEXT column record.  The slot a column advance leaves
+  // (refill target) is recomputed from it as a temporary, so no register an in-flight
+  // LDGSTS still has to read is overwritten right after it (a WAR stall on the MIO queue)
+  uint32_t cnext;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(cnext) : "r"(cslot + CS), "n"(WRAP), "r"(cslot));
   uint32_t rnext = smem_u32(F + k0 * SF);
   ST tr, vr, tc, vc;
   lds_rec(rnext, tr, vr);
-  lds_rec(cprev, tc, vc);
+  lds_rec(cslot, tc, vc);
   rnext += RS;
   // X/Y walk (see lane_walk) with the column cursor's identity carried in xc: X is the
   // cursor whose piece ends first; when the roles swap, X becomes the other cursor.
@@ -572,15 +581,14 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
       acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(tn, t)));
     }
     t = tn;
-    // slot addresses recomputed from jc each step (no loop-carried register is read by
-    // the in-flight LDGSTS, so nothing waits for the MIO queue to release it)
-    const uint32_t slot_cur = ring + (uint32_t)(jc & (D - 1)) * CS;
-    const uint32_t slot_nxt = ring + (uint32_t)((jc + 1) & (D - 1)) * CS;
-    const uint32_t addr = xc ? slot_nxt : rnext;
-    if (xc) {  // the column advances: refill the slot it leaves with record jc + D
-      const uint32_t r = (uint32_t)min(jc + D, ng - 1);
-      cp_async_rec<sizeof(RT)>(slot_cur, gb + r * RB);
-      ++jc;
+    const uint32_t addr = xc ? cnext : rnext;
+    if (xc) {  // the column advances: refill the slot it leaves, D records ahead
+      uint32_t left, nn;  // ((x +- CS) & WRAP) | (x & ~WRAP): one LOP3 each
+      asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(left) : "r"(cnext + (D - 1) * CS), "n"(WRAP), "r"(cnext));
+      asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(nn) : "r"(cnext + CS), "n"(WRAP), "r"(cnext));
+      cp_async_rec<sizeof(RT)>(left, gb + boff);
+      boff = min(boff + RB, boff_last);
+      cnext = nn;
     } else {
       rnext += RS;
     }
@@ -593,9 +601,6 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
     vy = sw ? nv : vy;
     xc = xc != sw;
   };
-  // one commit group per two steps: a record read at step s was requested at step
-  // <= s - (D - 1), i.e. in a group at least 3 groups old, so waiting until <= 2 groups
-  // are pending before each pair of steps covers both
   int s = 0;
 #pragma unroll 2
   for (; s + 1 < steps; s += 2) {
@@ -627,10 +632,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   __shared__ uint64_t bar;
   __shared__ int s_item;
   const int tid = threadIdx.x;
-  // the lane's prefetch ring at the top of the dynamic shared memory (slot 0 address)
-  const uint32_t ring = smem_u32(smem) + dynamic_smem_bytes() -
-                        (uint32_t)(kRingSlots * kTileThreads * sizeof(RT)) +
-                        (uint32_t)(tid * sizeof(RT));
+  // the prefetch rings at the top of the dynamic shared memory (1 KB aligned); this
+  // lane's slot 0
+  const uint32_t ring =
+      ((smem_u32(smem) + dynamic_smem_bytes() -
+        (uint32_t)(kRingSlots * kTileThreads * sizeof(RT))) & ~(kRingAlign - 1)) +
+      (uint32_t)(tid / GW) * (kRingSlots * 128u) + (uint32_t)(tid % GW) * (uint32_t)sizeof(RT);
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
