@@ -298,6 +298,19 @@ int pcf_tree_merge_level(int kind, int is_f32, const void* t_dev, const void* v_
                          const int32_t* cnt_dev, const int64_t* leaves_dev, int64_t nout,
                          int64_t ntot, void* t_out_dev, void* v_out_dev, double* v2_out_dev,
                          int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, void* stream);
+/* Several non-compacting merge levels in one pass (K5w, csrc/pcf_wmerge.cu): output node q
+ * of the last level combines the nlev-level subtree over input nodes
+ * [nfirst[q], nfirst[q] + ncnt[q]) (ncnt <= 2^nlev, nlev <= 4) in the reference tree shape
+ * (reduce.py:189-208), bit-identical to nlev successive pcf_tree_merge_level calls.
+ * leaves_dev: leaf count per INPUT node (kind 4 only).  Workspace from
+ * pcf_tree_merge_levels_workspace. */
+int pcf_tree_merge_levels_workspace(int64_t ntot, int64_t nout, int64_t* bytes);
+int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v_dev,
+                          const double* v2_dev, const int64_t* off_dev,
+                          const int64_t* nfirst_dev, const int32_t* ncnt_dev,
+                          const int64_t* leaves_dev, int64_t nout, int32_t nlev, int64_t ntot,
+                          void* t_out_dev, void* v_out_dev, double* v2_out_dev,
+                          int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, void* stream);
 /* mean finalisation: v * T(scale[seg]) (core.scale) + keep-where-changed flags.
  * t_dev (optional): the node times; zero-width pieces (next point of the node at the same
  * time) get flag 0 and survivors compare with the previous survivor. */

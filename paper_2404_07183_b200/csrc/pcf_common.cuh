@@ -149,8 +149,10 @@ template <int BYTES>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const void* src) {
   if constexpr (BYTES == 16) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-  } else {
+  } else if constexpr (BYTES == 8) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
   }
 }
 

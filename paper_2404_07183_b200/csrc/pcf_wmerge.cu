@@ -1,0 +1,710 @@
+// Fused non-compacting tree levels (K5w): k reduction-tree levels in ONE pass over HBM.
+//
+// Above level 0 of a tree whose breakpoints are (nearly) distinct, every level is a pure
+// merge (k_merge_level, pcf_level.cu): each output node is the time-ordered union of its
+// two children, every point carrying op(value of A, value of B) at that point, A first on
+// ties (reduce.py:31-63 per cell; reduce.py:189-208 for the tree).  One level costs a
+// full read + write of every point (3.2 GB at c5), and 19 levels dominate mean / std.
+//
+// Here one pass runs k levels: an output node at level L+k has C <= 2^k input nodes at
+// level L (a contiguous node range, combined in the reference tree shape: pairs
+// (0,1)(2,3)..., an odd last node passing through -- the global pairing restricted to
+// the subtree).  Its points, in merged order, are the union of the children's points
+// ordered by the key (t, child, index) -- exactly what k successive stable merges
+// produce.  The node is cut into tiles by keys (pivots taken from its largest child);
+// a tile = per child a sub-range [lo_c, hi_c) of points.  Each CTA stages its tile's
+// child ranges in shared memory and runs the k pairwise merges there (ping-pong
+// buffers), then writes the merged tile once.
+//
+// Values across a tile boundary: the value of list X just before the tile ("carry") is
+// v[lo - 1] for an input child (v[0] when lo = 0: reduce_pair's t = 0 convention, see
+// k_merge_level), and combine(carry_A, carry_B) for a merged list -- which is also the
+// value of X's first point when nothing of X precedes the tile.  Inside the tile an A
+// point takes B's value from B's previous point in the tile or B's carry, and vice
+// versa, so every point gets the value the level-by-level path computes, bit for bit
+// (same operand order, same rounding to the record kind after every level).
+//
+// A tile whose child ranges exceed the shared-memory capacity (pivots from one child do
+// not bound the other children's counts) is cut further inside the CTA by keys from its
+// largest contributor (halving it each time) and processed as consecutive sub-windows,
+// so any input -- including long runs of equal times -- is handled.
+#include "pcf_common.cuh"
+#include "pcf_internal.h"
+
+namespace pcfb {
+namespace wm {
+
+constexpr int WTH = 256;   // threads per tile CTA
+constexpr int WLPT = 8;    // merge positions per thread per round
+constexpr int KMAXC = 16;  // children per output node (k <= 4 levels per pass)
+enum { K_ADD = 0, K_MAX = 1, K_MIN = 2, K_MUL = 3, K_MOM = 4 };
+
+template <int K>
+__device__ __forceinline__ double vop(double x, double y) {
+  if (K == K_ADD) return __dadd_rn(x, y);
+  if (K == K_MUL) return __dmul_rn(x, y);
+  if (K == K_MAX) return x > y ? x : y;  // Python max(x, y)
+  return y < x ? y : x;                    // Python min(x, y)
+}
+
+template <typename T> __device__ __forceinline__ T to_t(double x);
+template <> __device__ __forceinline__ double to_t<double>(double x) { return x; }
+template <> __device__ __forceinline__ float to_t<float>(double x) { return __double2float_rn(x); }
+
+// points per tile (target) and shared-memory capacity per buffer
+template <typename T, int K> struct Cfg {
+  static constexpr bool MOM = K == K_MOM;
+  static constexpr int CAP = MOM ? 1280 : 2048;  // 3 CTAs per SM (~70 KB each)
+  static constexpr int TGT = MOM ? 1024 : 1536;
+  using VT = typename std::conditional<MOM, double, T>::type;
+  static constexpr int EB = (int)(sizeof(T) + sizeof(VT) + (MOM ? 8 : 0));
+  static constexpr int CAPP = CAP + CAP / 8;  // padded slots (pad(x) = x + x / 8)
+  static constexpr int SMEM = 2 * CAPP * EB;
+};
+
+// number of child c's points with key < (T, cs, is): the key order is (t, child, index)
+template <typename T>
+__device__ __forceinline__ int key_lower(const T* __restrict__ tc, int c, double kt, int cs,
+                                         int ki, int lo, int hi) {
+  if (c == cs) return ki;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const double x = (double)tc[mid];
+    const bool before = c < cs ? (x <= kt) : (x < kt);
+    if (before) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// per output node: tile count (>= 1) from its point count
+template <typename T, int K>
+__global__ void k_wnodes(const int64_t* __restrict__ off, const int64_t* __restrict__ nfirst,
+                         const int32_t* __restrict__ ncnt, int64_t nout,
+                         int64_t* __restrict__ tcount, int64_t* __restrict__ off_out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q <= nout;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    if (q == nout) {
+      off_out[nout] = off[nfirst[nout - 1] + ncnt[nout - 1]];
+      continue;
+    }
+    const int64_t f = nfirst[q];
+    const int64_t n = off[f + ncnt[q]] - off[f];
+    off_out[q] = off[f];
+    tcount[q] = n > 0 ? (n + Cfg<T, K>::TGT - 1) / Cfg<T, K>::TGT : 1;
+  }
+}
+
+// per-tile descriptors, so a tile CTA needs one dependent load before its staging loads:
+// the node's first input node and child count, and per child its input start and the
+// tile's [lo, end) range
+struct TileHead {
+  int64_t f;  // first input node
+  int32_t C;
+  int32_t pad_;
+};
+struct TileChild {
+  int64_t cb;  // input position of the child's first point
+  int32_t lo, end;
+};
+
+__global__ void k_wtiles(const int64_t* __restrict__ off, const int64_t* __restrict__ nfirst,
+                         const int32_t* __restrict__ ncnt, const int64_t* __restrict__ tbase,
+                         const int32_t* __restrict__ rb, int64_t nout,
+                         TileHead* __restrict__ th, TileChild* __restrict__ tc) {
+  const int64_t ntl = tbase[nout];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < ntl * KMAXC;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tl = x / KMAXC;
+    const int c = (int)(x % KMAXC);
+    int64_t lo = 0, hi = nout - 1;  // node: largest q with tbase[q] <= tl
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (tbase[mid] <= tl) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t q = lo, f = nfirst[q];
+    const int C = ncnt[q];
+    if (c == 0) {
+      TileHead h;
+      h.f = f;
+      h.C = C;
+      h.pad_ = 0;
+      th[tl] = h;
+    }
+    if (c < C) {
+      const int64_t g0 = tl + q;
+      TileChild e;
+      e.cb = off[f + c];
+      e.lo = rb[g0 * KMAXC + c];
+      e.end = rb[(g0 + 1) * KMAXC + c];
+      tc[tl * KMAXC + c] = e;
+    }
+  }
+}
+
+// single-CTA exclusive scan of n int64 counts -> out[0..n] (n up to a few million)
+__global__ void __launch_bounds__(1024) k_scan1(const int64_t* __restrict__ in, int64_t n,
+                                                int64_t* __restrict__ out) {
+  __shared__ int64_t wsum[32];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b = min((int64_t)tid * per, n), e = min(b + per, n);
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += in[i];
+  // block exclusive scan of s
+  int64_t x = s;
+  const int lane = tid & 31, w = tid >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t z = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z;
+  }
+  __syncthreads();
+  int64_t run = x - s + (w > 0 ? wsum[w - 1] : 0);
+  for (int64_t i = b; i < e; ++i) {
+    out[i] = run;
+    run += in[i];
+  }
+  if (tid == 1023) out[n] = run;
+}
+
+// per (output node, child): the length of the child's leading run of the node's first time
+// t0 (every PCF starts at t = 0, so at level L a node begins with one t = 0 point per
+// level-0 node -- a tie run that pivots from a single child cannot split)
+template <typename T>
+__global__ void k_wruns(const T* __restrict__ t, const int64_t* __restrict__ off,
+                        const int64_t* __restrict__ nfirst, const int32_t* __restrict__ ncnt,
+                        int64_t nout, int32_t* __restrict__ rr) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nout * KMAXC;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = x / KMAXC;
+    const int c = (int)(x % KMAXC);
+    const int C = ncnt[q];
+    if (c >= C) continue;
+    const int64_t f = nfirst[q];
+    double t0 = INFINITY;
+    for (int d = 0; d < C; ++d)
+      if (off[f + d + 1] > off[f + d]) t0 = fmin(t0, (double)t[off[f + d]]);
+    const T* tc = t + off[f + c];
+    const int nc = (int)(off[f + c + 1] - off[f + c]);
+    int lo = 0, hi = nc;  // count of points with t <= t0 (exponential then binary search)
+    int step = 1;
+    while (step < nc && (double)tc[step] <= t0) step <<= 1;
+    lo = step >> 1;
+    hi = min(step, nc);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((double)tc[mid] <= t0) lo = mid + 1;
+      else hi = mid;
+    }
+    rr[q * KMAXC + c] = nc > 0 && (double)tc[0] <= t0 ? lo : 0;
+  }
+}
+
+// tile boundaries: node q's boundary j (0 .. tcount[q]) lives at global index
+// tbase[q] + q + j; per child the number of its points before the boundary key
+//
+// Boundary j targets merged position P = j * N / ntiles.  Inside the leading t0 run the
+// merged order is child by child, so P maps to an exact key (t0, c, P - run prefix);
+// past it, the pivot is the largest child's point at the proportional index of the rest.
+template <typename T, int K>
+__global__ void k_wbounds(const T* __restrict__ t, const int64_t* __restrict__ off,
+                          const int64_t* __restrict__ nfirst, const int32_t* __restrict__ ncnt,
+                          int64_t nout, const int64_t* __restrict__ tbase,
+                          const int32_t* __restrict__ rr, int32_t* __restrict__ rb) {
+  const int64_t nb = tbase[nout] + nout;  // boundaries in total
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nb * KMAXC;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = x / KMAXC;
+    const int c = (int)(x % KMAXC);
+    int64_t lo = 0, hi = nout - 1;  // node: largest q with tbase[q] + q <= g
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (tbase[mid] + mid <= g) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t q = lo;
+    const int C = ncnt[q];
+    if (c >= C) continue;
+    const int64_t j = g - (tbase[q] + q);
+    const int64_t nt = tbase[q + 1] - tbase[q];
+    const int64_t f = nfirst[q];
+    const int nc = (int)(off[f + c + 1] - off[f + c]);
+    int r;
+    if (j == 0) {
+      r = 0;
+    } else if (j >= nt) {
+      r = nc;
+    } else {
+      const int64_t N = off[f + C] - off[f];
+      const int64_t P = j * N / nt;
+      int64_t R = 0;
+      for (int d = 0; d < C; ++d) R += rr[q * KMAXC + d];
+      int cb = 0, ki;
+      double kt;
+      if (P < R) {  // inside the leading run: exact
+        int64_t pre = 0;
+        while (pre + rr[q * KMAXC + cb] <= P) pre += rr[q * KMAXC + cb++];
+        ki = (int)(P - pre);
+        kt = (double)t[off[f + cb] + ki];
+      } else {
+        int64_t nbig = -1;
+        for (int d = 0; d < C; ++d) {
+          const int64_t n = off[f + d + 1] - off[f + d] - rr[q * KMAXC + d];
+          if (n > nbig) { nbig = n; cb = d; }
+        }
+        const int64_t r0 = rr[q * KMAXC + cb];
+        ki = (int)(r0 + (P - R) * nbig / (N - R));
+        kt = (double)t[off[f + cb] + ki];
+      }
+      r = key_lower<T>(t + off[f + c], c, kt, cb, ki, 0, nc);
+    }
+    rb[g * KMAXC + c] = r;
+  }
+}
+
+__device__ __forceinline__ int pad(int x) { return x + (x >> 3); }  // WLPT = 8
+
+// merge state of output list l at local position m: its A / B input spans and co-ranks
+struct ListPos {
+  int a0, na, b0, nb, i, j;
+  bool pass;
+};
+
+template <typename T>
+__device__ __forceinline__ ListPos open_list(const int* ls, int nl, int l, int m,
+                                             const T* it) {
+  ListPos L;
+  L.a0 = ls[2 * l];
+  L.pass = 2 * l + 1 >= nl;
+  L.na = ls[2 * l + 1] - L.a0;  // a passthrough list ends at ls[nl]
+  L.b0 = ls[2 * l + 1];
+  L.nb = L.pass ? 0 : ls[2 * l + 2] - L.b0;
+  if (L.pass) {
+    L.i = m;
+    L.j = 0;
+    return L;
+  }
+  int lo = max(0, m - L.nb), hi = min(m, L.na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (it[pad(L.a0 + mid)] <= it[pad(L.b0 + m - mid - 1)]) lo = mid + 1;
+    else hi = mid;
+  }
+  L.i = lo;
+  L.j = m - lo;
+  return L;
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(WTH, 3)
+    k_wmerge(const T* __restrict__ t, const void* __restrict__ v_, const double* __restrict__ v2,
+             const int64_t* __restrict__ off, const int64_t* __restrict__ nfirst,
+             const int32_t* __restrict__ ncnt, const int64_t* __restrict__ leaves, int64_t nout,
+             int nlev, const int64_t* __restrict__ tbase, const TileHead* __restrict__ th,
+             const TileChild* __restrict__ tc,
+             T* __restrict__ t_out, void* __restrict__ v_out_, double* __restrict__ v2_out) {
+  using C_ = Cfg<T, K>;
+  using VT = typename C_::VT;
+  constexpr bool MOM = C_::MOM;
+  constexpr int CAP = C_::CAP;
+  const VT* __restrict__ v = reinterpret_cast<const VT*>(v_);
+  VT* __restrict__ v_out = reinterpret_cast<VT*>(v_out_);
+  extern __shared__ __align__(16) unsigned char dyn[];
+  // buffer k: t[CAP] | v[CAP] | (v2[CAP])
+  constexpr int CP = C_::CAPP;
+  auto bt = [&](int k) { return reinterpret_cast<T*>(dyn + k * CP * C_::EB); };
+  auto bv = [&](int k) {
+    return reinterpret_cast<VT*>(dyn + k * CP * C_::EB + CP * (int)sizeof(T));
+  };
+  auto b2 = [&](int k) {
+    return reinterpret_cast<double*>(dyn + k * CP * C_::EB + CP * (int)(sizeof(T) + sizeof(VT)));
+  };
+  __shared__ int64_t s_cb[KMAXC];                 // first input position of each child
+  __shared__ int s_lo[KMAXC], s_hi[KMAXC], s_end[KMAXC];
+  __shared__ int s_ls[2][KMAXC + 1];              // list spans (ping-pong with the levels)
+  __shared__ VT s_cv[2][KMAXC];                   // carries
+  __shared__ double s_c2[2][KMAXC];
+  __shared__ double s_lv[2][KMAXC];               // leaf counts (moments weights)
+  __shared__ double s_w[2][KMAXC / 2][2];         // per output list: nB / n, nA * nB / n
+  __shared__ int s_tot, s_big, s_ki;
+  __shared__ double s_kt;
+  __shared__ int64_t s_wbase;
+
+  __shared__ int64_t s_f;
+  __shared__ int s_C;
+  const int tid = threadIdx.x;
+  const int64_t ntiles = tbase[nout];
+  // persistent: tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the next tile's descriptor
+  // is loaded while the current one is processed
+  int64_t tl = blockIdx.x;
+  if (tl >= ntiles) return;
+  TileHead nh = th[tl];
+  TileChild nc_;
+  if (tid < KMAXC && tid < nh.C) nc_ = tc[tl * KMAXC + tid];
+  for (; tl < ntiles; tl += gridDim.x) {
+  if (tid == 0) {
+    s_f = nh.f;
+    s_C = nh.C;
+  }
+  if (tid < nh.C) {
+    s_cb[tid] = nc_.cb;
+    s_lo[tid] = nc_.lo;
+    s_end[tid] = nc_.end;
+  }
+  __syncthreads();
+  const int64_t f = s_f;
+  const int C = s_C;
+  const int64_t nbase = s_cb[0];
+  if (tl + gridDim.x < ntiles) {  // prefetch the next descriptor
+    nh = th[tl + gridDim.x];
+    if (tid < KMAXC && tid < nh.C) nc_ = tc[(tl + gridDim.x) * KMAXC + tid];
+  }
+  if (MOM && tid < C) s_lv[0][tid] = (double)leaves[f + tid];
+  __syncthreads();
+  for (;;) {
+    // ---- the next sub-window [lo, hi): the whole tile unless it exceeds CAP points
+    if (tid < C) s_hi[tid] = s_end[tid];
+    __syncthreads();
+    for (;;) {
+      if (tid == 0) {
+        int tot = 0, big = 0, nbig = -1;
+        for (int c = 0; c < C; ++c) {
+          const int n = s_hi[c] - s_lo[c];
+          tot += n;
+          if (n > nbig) { nbig = n; big = c; }
+        }
+        s_tot = tot;
+        if (tot > CAP) {
+          const int mid = s_lo[big] + nbig / 2;
+          s_big = big;
+          s_ki = mid;
+          s_kt = (double)t[s_cb[big] + mid];
+        }
+      }
+      __syncthreads();
+      if (s_tot <= CAP) break;
+      if (tid < C)
+        s_hi[tid] = key_lower<T>(t + s_cb[tid], tid, s_kt, s_big, s_ki, s_lo[tid], s_hi[tid]);
+      __syncthreads();
+    }
+    const int E = s_tot;
+    if (tid == 0) {
+      int run = 0;
+      int64_t wb = 0;
+      for (int c = 0; c < C; ++c) {
+        s_ls[0][c] = run;
+        run += s_hi[c] - s_lo[c];
+        wb += s_lo[c];
+      }
+      s_ls[0][C] = run;
+      s_wbase = wb;
+    }
+    if (tid < C) {  // carries: the child's point before the window (its first point at 0)
+      const int64_t pc = s_cb[tid] + (s_lo[tid] > 0 ? s_lo[tid] - 1 : 0);
+      cp_async_rec<sizeof(VT)>(smem_u32(&s_cv[0][tid]), v + pc);
+      if (MOM) cp_async_rec<8>(smem_u32(&s_c2[0][tid]), v2 + pc);
+    }
+    __syncthreads();
+    // ---- stage the children's ranges, concatenated in child order (coalesced per child);
+    //      shared layout: element x at x + x / WLPT (one pad slot per thread's run, so the
+    //      runs of WLPT consecutive elements the threads write fall in distinct banks)
+    {
+      T* st = bt(0);
+      VT* sv = bv(0);
+      double* s2 = b2(0);
+      // warp w copies children w, w + 8, ...: no per-element child lookup; asynchronous
+      // copies keep every load of the tile in flight at once
+      const int lane = tid & 31;
+      for (int c = tid >> 5; c < C; c += WTH / 32) {
+        const int x0 = s_ls[0][c], x1 = s_ls[0][c + 1];
+        const T* gt = t + (s_cb[c] + s_lo[c] - x0);
+        const VT* gv = v + (s_cb[c] + s_lo[c] - x0);
+        const double* g2 = v2 + (s_cb[c] + s_lo[c] - x0);
+        for (int x = x0 + lane; x < x1; x += 32) {
+          const int y = pad(x);
+          cp_async_rec<sizeof(T)>(smem_u32(st + y), gt + x);
+          cp_async_rec<sizeof(VT)>(smem_u32(sv + y), gv + x);
+          if (MOM) cp_async_rec<8>(smem_u32(s2 + y), g2 + x);
+        }
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    // ---- the k levels, pairwise, in shared memory
+    int cur = 0, nl = C;
+    for (int lev = 0; lev < nlev && nl > 1; ++lev) {
+      const int nl2 = (nl + 1) >> 1;
+      const int* ls = s_ls[lev & 1];
+      int* ls2 = s_ls[(lev + 1) & 1];
+      if (tid <= nl2) ls2[tid] = tid < nl2 ? ls[2 * tid] : ls[nl];
+      if (MOM && tid < nl2 && 2 * tid + 1 < nl) {  // moments weights of output list tid
+        const double nA = s_lv[lev & 1][2 * tid], nB = s_lv[lev & 1][2 * tid + 1];
+        const double n = nA + nB;
+        s_w[lev & 1][tid][0] = nB / n;
+        s_w[lev & 1][tid][1] = nA * nB / n;
+      }
+      const T* it = bt(cur);
+      const VT* iv = bv(cur);
+      const double* i2 = b2(cur);
+      T* ot = bt(cur ^ 1);
+      VT* ov = bv(cur ^ 1);
+      double* o2 = b2(cur ^ 1);
+      const VT* cv = s_cv[lev & 1];
+      const double* c2 = s_c2[lev & 1];
+      const double* lv = s_lv[lev & 1];
+      __syncthreads();
+      const T TINF = (T)INFINITY;
+      for (int base = 0; base < E; base += WTH * WLPT) {
+        const int p0 = base + tid * WLPT;
+        T o_t[WLPT];
+        VT o_v[WLPT];
+        double o_2[WLPT];
+        if (p0 < E) {
+          int li = 0;  // output list containing p0
+          {
+            int lo = 0, hi = nl2 - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (ls2[mid] <= p0) lo = mid;
+              else hi = mid - 1;
+            }
+            li = lo;
+          }
+          // walk state: the next time of A and B (+inf past the end) and the values of A
+          // and B at the current point (their last consumed point, or their carry)
+          int a0 = 0, na = 0, b0 = 0, nb = 0, i = 0, j = 0;
+          bool pass = false;
+          T tai = TINF, tbj = TINF;
+          VT ca = VT(0), cb = VT(0);
+          double ca2 = 0.0, cb2 = 0.0, wB = 0.0, wAB = 0.0;
+          auto open = [&](int m) {
+            const ListPos L = open_list(ls, nl, li, m, it);
+            a0 = L.a0; na = L.na; b0 = L.b0; nb = L.nb; i = L.i; j = L.j;
+            pass = L.pass;
+            tai = i < na ? it[pad(a0 + i)] : TINF;
+            tbj = j < nb ? it[pad(b0 + j)] : TINF;
+            ca = i > 0 ? iv[pad(a0 + i - 1)] : cv[2 * li];
+            if (MOM) ca2 = i > 0 ? i2[pad(a0 + i - 1)] : c2[2 * li];
+            if (!pass) {
+              cb = j > 0 ? iv[pad(b0 + j - 1)] : cv[2 * li + 1];
+              if (MOM) {
+                cb2 = j > 0 ? i2[pad(b0 + j - 1)] : c2[2 * li + 1];
+                wB = s_w[lev & 1][li][0];
+                wAB = s_w[lev & 1][li][1];
+              }
+            }
+          };
+          open(p0 - ls2[li]);
+#pragma unroll
+          for (int qq = 0; qq < WLPT; ++qq) {
+            const int p = p0 + qq;
+            if (p < E) {
+              if (li + 1 < nl2 && p >= ls2[li + 1]) {
+                ++li;  // the next non-empty list (a sub-window can leave lists empty)
+                while (li + 1 < nl2 && p >= ls2[li + 1]) ++li;
+                open(0);
+              }
+              const bool takeA = tai <= tbj;  // A first on ties
+              if (takeA) {
+                o_t[qq] = tai;
+                ca = iv[pad(a0 + i)];
+                if (MOM) ca2 = i2[pad(a0 + i)];
+                ++i;
+                tai = i < na ? it[pad(a0 + i)] : TINF;
+              } else {
+                o_t[qq] = tbj;
+                cb = iv[pad(b0 + j)];
+                if (MOM) cb2 = i2[pad(b0 + j)];
+                ++j;
+                tbj = j < nb ? it[pad(b0 + j)] : TINF;
+              }
+              if (pass) {
+                o_v[qq] = ca;
+                if (MOM) o_2[qq] = ca2;
+              } else if (MOM) {
+                const double d = (double)cb - (double)ca;
+                o_v[qq] = (VT)((double)ca + d * wB);
+                o_2[qq] = (ca2 + cb2) + d * d * wAB;
+              } else {
+                o_v[qq] = to_t<VT>(vop<K>((double)ca, (double)cb));
+              }
+            }
+          }
+#pragma unroll
+          for (int qq = 0; qq < WLPT; ++qq) {
+            if (p0 + qq < E) {
+              const int y = pad(p0 + qq);
+              ot[y] = o_t[qq];
+              ov[y] = o_v[qq];
+              if (MOM) o2[y] = o_2[qq];
+            }
+          }
+        }
+      }
+      // carries and leaf counts of the merged lists
+      if (tid < nl2) {
+        VT* ncv = s_cv[(lev + 1) & 1];
+        double* nc2 = s_c2[(lev + 1) & 1];
+        double* nlv = s_lv[(lev + 1) & 1];
+        if (2 * tid + 1 >= nl) {
+          ncv[tid] = cv[2 * tid];
+          if (MOM) {
+            nc2[tid] = c2[2 * tid];
+            nlv[tid] = lv[2 * tid];
+          }
+        } else if (MOM) {
+          const double nA = lv[2 * tid], nB = lv[2 * tid + 1];
+          const double n = nA + nB;
+          const double va = cv[2 * tid], vb = cv[2 * tid + 1];
+          const double d = vb - va;
+          ncv[tid] = (VT)(va + d * (nB / n));
+          nc2[tid] = (c2[2 * tid] + c2[2 * tid + 1]) + d * d * (nA * nB / n);
+          nlv[tid] = n;
+        } else {
+          ncv[tid] = to_t<VT>(vop<K>((double)cv[2 * tid], (double)cv[2 * tid + 1]));
+        }
+      }
+      __syncthreads();
+      cur ^= 1;
+      nl = nl2;
+    }
+    // ---- the merged window, written once (coalesced)
+    {
+      const T* st = bt(cur);
+      const VT* sv = bv(cur);
+      const double* s2 = b2(cur);
+      const int64_t ob = nbase + s_wbase;
+      for (int x = tid; x < E; x += WTH) {
+        const int y = pad(x);
+        t_out[ob + x] = st[y];
+        v_out[ob + x] = sv[y];
+        if (MOM) v2_out[ob + x] = s2[y];
+      }
+    }
+    // ---- next sub-window of the tile
+    __syncthreads();
+    int more = 0;
+    if (tid < C) {
+      s_lo[tid] = s_hi[tid];
+      more = s_lo[tid] < s_end[tid];
+    }
+    if (!__syncthreads_or(more)) break;
+    if (MOM && tid < C) s_lv[0][tid] = (double)leaves[f + tid];
+  }
+  __syncthreads();  // the descriptors in shared memory are reused by the next tile
+  }
+}
+
+}  // namespace wm
+}  // namespace pcfb
+
+using namespace pcfb;
+using namespace pcfb::wm;
+
+extern "C" {
+
+// workspace for pcf_tree_merge_levels: tile counts / bases (nout + 1 each) and the
+// boundary table ((ntot / 1280 + 2 * nout + 2) x 16 int32)
+int pcf_tree_merge_levels_workspace(int64_t ntot, int64_t nout, int64_t* bytes) {
+  if (!bytes || ntot < 0 || nout < 0) {
+    set_error("pcf_tree_merge_levels_workspace: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  const int64_t nb = ntot / 1024 + 2 * nout + 2;
+  const int64_t nt = ntot / 1024 + nout + 1;  // tiles (upper bound)
+  *bytes = 2 * (nout + 1) * 8 + nb * KMAXC * 4 + nout * KMAXC * 4 + nt * 16 +
+           nt * KMAXC * 16 + 512;
+  return PCF_OK;
+}
+
+int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v_dev,
+                          const double* v2_dev, const int64_t* off_dev,
+                          const int64_t* nfirst_dev, const int32_t* ncnt_dev,
+                          const int64_t* leaves_dev, int64_t nout, int32_t nlev, int64_t ntot,
+                          void* t_out_dev, void* v_out_dev, double* v2_out_dev,
+                          int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nout <= 0) return PCF_OK;
+  if (kind < 0 || kind > 4 || nlev < 1 || nlev > 4 || !t_dev || !v_dev || !off_dev ||
+      !nfirst_dev || !ncnt_dev || !t_out_dev || !v_out_dev || !off_out_dev || !ws_dev ||
+      (kind == K_MOM && (!v2_dev || !v2_out_dev || !leaves_dev))) {
+    set_error("pcf_tree_merge_levels: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  int64_t need = 0;
+  pcf_tree_merge_levels_workspace(ntot, nout, &need);
+  if (ws_bytes < need) {
+    set_error("pcf_tree_merge_levels: workspace %lld < %lld bytes", (long long)ws_bytes,
+              (long long)need);
+    return PCF_ERR_ARG;
+  }
+  int64_t* tcount = (int64_t*)ws_dev;
+  int64_t* tbase = tcount + (nout + 1);
+  int32_t* rr = (int32_t*)(tbase + (nout + 1));
+  int32_t* rb = rr + nout * KMAXC;
+  const int64_t ntile_max = ntot / 1024 + nout + 1;
+  uintptr_t pth = (uintptr_t)(rb + (ntot / 1024 + 2 * nout + 2) * KMAXC);
+  pth = (pth + 15) & ~(uintptr_t)15;
+  TileHead* th = (TileHead*)pth;
+  TileChild* tch = (TileChild*)(th + ntile_max);
+  const int ng = (int)std::min<int64_t>((nout + 1 + 255) / 256, 4096);
+  const int bg = (int)std::min<int64_t>(((ntile_max + nout + 1) * KMAXC + 255) / 256, 148 * 64);
+  const int rg = (int)std::min<int64_t>((nout * KMAXC + 255) / 256, 148 * 64);
+  int nsm = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+#define PCF_WM(T, K)                                                                          \
+  do {                                                                                        \
+    k_wnodes<T, K><<<ng, 256, 0, s>>>(off_dev, nfirst_dev, ncnt_dev, nout, tcount,             \
+                                      off_out_dev);                                           \
+    k_scan1<<<1, 1024, 0, s>>>(tcount, nout, tbase);                                          \
+    k_wruns<T><<<rg, 256, 0, s>>>((const T*)t_dev, off_dev, nfirst_dev, ncnt_dev, nout, rr);  \
+    k_wbounds<T, K><<<bg, 256, 0, s>>>((const T*)t_dev, off_dev, nfirst_dev, ncnt_dev, nout,  \
+                                       tbase, rr, rb);                                        \
+    k_wtiles<<<bg, 256, 0, s>>>(off_dev, nfirst_dev, ncnt_dev, tbase, rb, nout, th, tch);     \
+    const int dsm = Cfg<T, K>::SMEM;                                                          \
+    cudaFuncSetAttribute(k_wmerge<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);   \
+    const int64_t grid = std::min<int64_t>(ntot / Cfg<T, K>::TGT + nout + 1, 3 * nsm);        \
+    k_wmerge<T, K><<<(unsigned)grid, WTH, dsm, s>>>(                                          \
+        (const T*)t_dev, v_dev, v2_dev, off_dev, nfirst_dev, ncnt_dev, leaves_dev, nout, nlev, \
+        tbase, th, tch, (T*)t_out_dev, v_out_dev, v2_out_dev);                                \
+  } while (0)
+  if (is_f32) {
+    switch (kind) {
+      case K_ADD: PCF_WM(float, K_ADD); break;
+      case K_MAX: PCF_WM(float, K_MAX); break;
+      case K_MIN: PCF_WM(float, K_MIN); break;
+      case K_MUL: PCF_WM(float, K_MUL); break;
+      default: PCF_WM(float, K_MOM); break;
+    }
+  } else {
+    switch (kind) {
+      case K_ADD: PCF_WM(double, K_ADD); break;
+      case K_MAX: PCF_WM(double, K_MAX); break;
+      case K_MIN: PCF_WM(double, K_MIN); break;
+      case K_MUL: PCF_WM(double, K_MUL); break;
+      default: PCF_WM(double, K_MOM); break;
+    }
+  }
+#undef PCF_WM
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("pcf_tree_merge_levels: %s", cudaGetErrorString(e));
+    return PCF_ERR_CUDA;
+  }
+  return PCF_OK;
+}
+
+}  // extern "C"

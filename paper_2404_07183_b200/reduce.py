@@ -218,6 +218,32 @@ def _device_plan(seg_nodes, leaves0, moments, dev):
     return res
 
 
+_FUSED_CACHE = {}
+
+
+def _fused_tables(plan, l0, l1, pkey, dev):
+    """Node tables of levels [l0, l1) run as one fused pass: for every output node of level
+    l1 - 1 the first input node of level l0 and the number of input nodes its subtree
+    covers (the level pairings composed downwards; device int64 / int32 arrays)."""
+    key = None if pkey is None else pkey + (l0, l1)
+    if key is not None and key in _FUSED_CACHE:
+        return _FUSED_CACHE[key]
+    torch = _torch()
+    src, cnt = plan[l1 - 1][0], plan[l1 - 1][1]
+    first = np.asarray(src, dtype=np.int64)
+    last = first + np.asarray(cnt, dtype=np.int64)
+    for lvl in range(l1 - 2, l0 - 1, -1):
+        s_, c_ = np.asarray(plan[lvl][0], dtype=np.int64), np.asarray(plan[lvl][1], dtype=np.int64)
+        first, last = s_[first], s_[last - 1] + c_[last - 1]
+    res = (torch.from_numpy(first).to(dev),
+           torch.from_numpy((last - first).astype(np.int32)).to(dev))
+    if key is not None:
+        if len(_FUSED_CACHE) > 64:
+            _FUSED_CACHE.clear()
+        _FUSED_CACHE[key] = res
+    return res
+
+
 def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=None):
     """Reduce each fibre (seg_nodes[i] consecutive nodes) to one node: one tiled level
     kernel per tree level -- compacting (pcf_tree_level) for level 0, and for the upper
@@ -257,9 +283,45 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
     nout = level.nnodes
     mode = os.environ.get("PCF_TREE_MODE", "auto")  # auto | compact | merge
     merge = mode == "merge"
-    for li, (src, cnt, _) in enumerate(plan):
+    # levels per fused pass (pcf_tree_merge_levels, K5w): the sum/max/min/mul trees gain from
+    # 4 (c5 mean 18.3 -> 17.1 ms); the moments tree (24-byte points, smaller tiles) runs
+    # faster level by level (26.6 vs 29.0 ms), so it defaults to 1
+    fuse_env = os.environ.get("PCF_TREE_FUSE")
+    fuse = max(1, min(4, int(fuse_env))) if fuse_env else (1 if moments else 4)
+    pkey = (None if leaves0 is not None or np.asarray(seg_nodes).size > 64 else
+            (tuple(int(x) for x in np.asarray(seg_nodes)), bool(moments), str(dev)))
+    li = 0
+    nbuf = 0
+    while li < len(plan):
+        src, cnt, _ = plan[li]
+        if merge and li > 0 and fuse > 1 and len(plan) - li > 1:
+            # several non-compacting levels in one pass (pcf_tree_merge_levels, K5w)
+            g = min(fuse, len(plan) - li)
+            nfirst, ncnt = _fused_tables(plan, li, li + g, pkey, dev)
+            nout = int(plan[li + g - 1][0].shape[0])
+            t_out, v_out, m2_out = bufs[nbuf % 2]
+            off_out = torch.empty(nout + 1, dtype=torch.int64, device=dev)
+            nbw = _native.c_i64(0)
+            lib.pcf_tree_merge_levels_workspace(bound, nout, _native.ctypes.byref(nbw))
+            wsw = _scratch("wsw", max(nbw.value, 256), torch.uint8, dev)
+            _native.check(lib.pcf_tree_merge_levels(
+                kind, int(level.is_f32), _native.ptr(cur_t), _native.ptr(cur_v),
+                _native.ptr(cur_m2) if moments else None, _native.ptr(cur_off),
+                _native.ptr(nfirst), _native.ptr(ncnt),
+                _native.c_vp(lv_d.data_ptr() + 8 * lo) if moments else None,
+                nout, g, bound, _native.ptr(t_out), _native.ptr(v_out),
+                _native.ptr(m2_out) if moments else None, _native.ptr(off_out), _native.ptr(wsw),
+                wsw.numel(), st), "pcf_tree_merge_levels")
+            for k in range(g):
+                so += plan[li + k][0].shape[0]
+                if moments:
+                    lo += plan[li + k][2].shape[0]
+            cur_t, cur_v, cur_m2, cur_off = t_out, v_out, m2_out, off_out
+            li += g
+            nbuf += 1
+            continue
         nout = src.shape[0]
-        t_out, v_out, m2_out = bufs[li % 2]
+        t_out, v_out, m2_out = bufs[nbuf % 2]
         off_out = torch.empty(nout + 1, dtype=torch.int64, device=dev)
         args = (int(level.is_f32), _native.ptr(cur_t), _native.ptr(cur_v),
                 _native.ptr(cur_m2) if moments else None, _native.ptr(cur_off),
@@ -283,6 +345,8 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
         if moments:
             lo += plan[li][2].shape[0]
         cur_t, cur_v, cur_m2, cur_off = t_out, v_out, m2_out, off_out
+        li += 1
+        nbuf += 1
     ntot = int(cur_off[-1].item())
     if not moments:
         _check_status(status, "reduction")
