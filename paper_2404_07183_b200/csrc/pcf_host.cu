@@ -95,10 +95,14 @@ cudaError_t copy_rows(const std::vector<int32_t>& perm, const std::vector<int32_
   for (size_t k = 0; k < n;) {
     size_t e = k + 1;
     while (e < n && o[e] == o[e - 1] + 1) ++e;
-    const cudaError_t rc = cudaMemcpy2DAsync(
-        hdst + (size_t)o[k] * (size_t)ld * es, (size_t)ld * es,
-        dsrc + (size_t)o[k] * row_bytes, row_bytes, row_bytes, e - k,
-        cudaMemcpyDeviceToHost, st);
+    char* h = hdst + (size_t)o[k] * (size_t)ld * es;
+    const char* d = dsrc + (size_t)o[k] * row_bytes;
+    // contiguous on both sides (one row, or ld == M): a plain 1-D copy
+    const cudaError_t rc =
+        (e - k == 1 || ld == M)
+            ? cudaMemcpyAsync(h, d, row_bytes * (e - k), cudaMemcpyDeviceToHost, st)
+            : cudaMemcpy2DAsync(h, (size_t)ld * es, d, row_bytes, row_bytes, e - k,
+                                cudaMemcpyDeviceToHost, st);
     if (rc != cudaSuccess) return rc;
     k = e;
   }
