@@ -311,6 +311,19 @@ int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v
                           const int64_t* leaves_dev, int64_t nout, int32_t nlev, int64_t ntot,
                           void* t_out_dev, void* v_out_dev, double* v2_out_dev,
                           int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, void* stream);
+/* Whole finalisation of a reduction tree's root level(s) in two tiled passes (no flag or
+ * scaled-value arrays in HBM): kind 0 = mean, v * T(scale[seg]) (core.scale + the final
+ * minimize_discretization, reduce.py:211-217); kind 1 = variance T(M2 * scale[seg]);
+ * kind 2 = std, T(sqrt(variance)) (reduce.py:220-238).  Zero-width pieces of non-compacting
+ * levels (equal times within a node) are dropped first.  src_dev: v (kind 0) or M2
+ * (float64, kinds 1-2); t_dev/off_dev: the level; nseg nodes.  Writes the kept points to
+ * t_out/v_out (record kind) and off_out[nseg+1]; status |= 1 on a non-finite value.
+ * Workspace from pcf_finalize_workspace. */
+int pcf_finalize_workspace(int64_t ntot, int64_t* bytes);
+int pcf_finalize(int kind, int is_f32, const void* src_dev, const void* t_dev,
+                 const int64_t* off_dev, int64_t nseg, const double* scale_dev, int64_t ntot,
+                 void* t_out_dev, void* v_out_dev, int64_t* off_out_dev, int32_t* status_dev,
+                 void* ws_dev, int64_t ws_bytes, void* stream);
 /* mean finalisation: v * T(scale[seg]) (core.scale) + keep-where-changed flags.
  * t_dev (optional): the node times; zero-width pieces (next point of the node at the same
  * time) get flag 0 and survivors compare with the previous survivor. */

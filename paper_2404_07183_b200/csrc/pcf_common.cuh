@@ -179,6 +179,38 @@ __device__ __forceinline__ uint32_t dynamic_smem_bytes() {
   return n;
 }
 
+// Exclusive prefix sum of one int per thread over a CTA of NT threads (NT a multiple of 32,
+// at most 1024); ws = shared scratch of NT / 32 ints.  Returns the thread's prefix and the
+// CTA total in *total.  Ends with a barrier, so ws may be reused right after.
+template <int NT>
+__device__ __forceinline__ int block_exclusive_sum(int x, int* ws, int* total) {
+  static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) ws[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int z = lane < NW ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < NW) ws[lane] = z;
+  }
+  __syncthreads();
+  const int before = w > 0 ? ws[w - 1] : 0;
+  *total = ws[NW - 1];
+  __syncthreads();
+  return before + inc - x;
+}
+
 // Largest count of x in [0, n) with key(x) <= a, for sorted keys (upper_bound).
 template <typename KeyF>
 __device__ __forceinline__ int upper_bound_count(int n, double a, KeyF key) {

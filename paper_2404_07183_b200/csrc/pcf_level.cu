@@ -21,8 +21,7 @@
 // Tiles whose nodes need several rounds (more than MAXSEG nodes) park their kept points
 // in a scratch region until the offset is known.  Node start offsets are stored
 // tile-relative and fixed up by k_fix_offsets.
-#define CCCL_IGNORE_DEPRECATED_API 1
-#include <cub/cub.cuh>
+#include <type_traits>
 #include "pcf_common.cuh"
 #include "pcf_internal.h"
 
@@ -106,8 +105,7 @@ __global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
   T* s_t = reinterpret_cast<T*>(dyn + WCAP * sizeof(VT) + (MOM ? WCAP * sizeof(double) : 0));
   __shared__ uint64_t s_bar;  // bulk-copy completion of the staged windows
   __shared__ int64_t s_next_node, s_round_end, s_tile, s_excl;
-  typedef cub::BlockScan<int, LTH> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int scan_ws[LTH / 32];
 
   const int tid = threadIdx.x;
   // Tiles are taken in order from an atomic counter, so every tile's predecessors are
@@ -201,7 +199,7 @@ __global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
                         : 0;
     }
     int woff, wtot;
-    Scan(scan_tmp).ExclusiveSum(la_p + lb_p, woff, wtot);
+    woff = block_exclusive_sum<LTH>(la_p + lb_p, scan_ws, &wtot);
     if (tid < nseg) {
       seg[tid].aoff = woff + (int)(seg[tid].ga & (U - 1));
       seg[tid].boff = woff + la_p + (int)(seg[tid].gb & (U - 1));
@@ -398,7 +396,7 @@ __global__ void __launch_bounds__(LTH, K == K_MOM ? 3 : 4)
     }
     const int nk = __popc(kmask);
     int koff, ktot;
-    Scan(scan_tmp).ExclusiveSum(nk, koff, ktot);
+    koff = block_exclusive_sum<LTH>(nk, scan_ws, &ktot);
     // node starts of this round: tile-local output index now, the tile's offset is added
     // by k_fix_offsets after the level (tile_excl)
     if (nsmask) {
@@ -553,8 +551,7 @@ __global__ void __launch_bounds__(MT, (K == K_MOM ? 3 : 4) * 256 / MT)
   T* s_t = reinterpret_cast<T*>(dyn + WCAP * sizeof(VT) + (MOM ? WCAP * sizeof(double) : 0));
   __shared__ uint64_t s_bar;
   __shared__ int64_t s_next_node, s_round_end;
-  typedef cub::BlockScan<int, MT> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int scan_ws[MT / 32];
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -627,7 +624,7 @@ __global__ void __launch_bounds__(MT, (K == K_MOM ? 3 : 4) * 256 / MT)
                         : 0;
     }
     int woff, wtot;
-    Scan(scan_tmp).ExclusiveSum(la_p + lb_p, woff, wtot);
+    woff = block_exclusive_sum<MT>(la_p + lb_p, scan_ws, &wtot);
     if (tid < nseg) {
       seg[tid].aoff = woff + (int)(seg[tid].ga & (U - 1));
       seg[tid].boff = woff + la_p + (int)(seg[tid].gb & (U - 1));

@@ -3,10 +3,11 @@
 //
 // The finalisation flags every point of the root node(s) -- keep where the scaled value
 // differs from the previous surviving point's (minimize_discretization), drop zero-width
-// pieces left by non-compacting levels -- and pcf_compact turns the flags into positions
-// (device exclusive scan) and scatters the kept points and the node offsets.
-#define CCCL_IGNORE_DEPRECATED_API 1
-#include <cub/cub.cuh>
+// pieces left by non-compacting levels.  pcf_finalize does it in two passes over tiles of
+// 4096 points (count the kept points per tile; single-CTA scan of the tile counts;
+// recompute and write the kept points through shared memory, coalesced), so neither the
+// scaled values nor the flags ever go to HBM.  pcf_compact (flags -> positions -> scatter)
+// uses the same tile scan.  No library scan on this path.
 #include "pcf_common.cuh"
 #include "pcf_internal.h"
 
@@ -139,9 +140,231 @@ __global__ void k_std_flag(const double* __restrict__ m2, const T* __restrict__ 
   }
 }
 
-struct Widen {
-  __host__ __device__ __forceinline__ int64_t operator()(int32_t x) const { return (int64_t)x; }
-};
+
+// ------------------------------------------------------------ tiled finalisation
+constexpr int FT = 256;           // threads per tile
+constexpr int FPT = 8;            // consecutive points per thread
+constexpr int FTILE = FT * FPT;   // points per tile
+
+// value of point q (kind 0: mean = v * T(scale); 1: variance T(M2 * scale); 2: std)
+template <typename T, int KIND>
+__device__ __forceinline__ T fin_value(const void* __restrict__ src, int64_t q, double sc) {
+  if (KIND == 0) {
+    const T* v = reinterpret_cast<const T*>(src);
+    return v[q] * to_t<T>(sc);
+  }
+  const double* m2 = reinterpret_cast<const double*>(src);
+  const T var = to_t<T>(m2[q] * sc);
+  return KIND == 2 ? to_t<T>(sqrt((double)var)) : var;
+}
+
+// point e: value and keep flag (first point of its node, or a value change against the
+// last survivor; zero-width pieces dropped).  seg: the node of e (found by the caller).
+template <typename T, int KIND>
+__device__ __forceinline__ bool fin_point(const void* __restrict__ src, const T* __restrict__ t,
+                                          int64_t e, int64_t sbeg, int64_t send, double sc,
+                                          T* val, bool* bad) {
+  const T x = fin_value<T, KIND>(src, e, sc);
+  *val = x;
+  if (zero_width(t, e, send)) return false;
+  if (!isfinite((double)x)) *bad = true;
+  const int64_t p = prev_survivor(t, e, sbeg);
+  return p < sbeg || x != fin_value<T, KIND>(src, p, sc);
+}
+
+// node of point e (largest k with off[k] <= e)
+__device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ off, int64_t nseg,
+                                          int64_t e) {
+  int64_t lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// A tile is FPT rows of FT consecutive points; warp w of row k handles 32 consecutive
+// points (coalesced loads), its keep flags are one ballot.  Point order = (row, warp, lane).
+template <typename T, int KIND>
+__global__ void __launch_bounds__(FT, 6) k_fin_count(const void* __restrict__ src,
+                                                  const T* __restrict__ t,
+                                                  const int64_t* __restrict__ off, int64_t nseg,
+                                                  const double* __restrict__ scale, int64_t ntot,
+                                                  int64_t* __restrict__ tsum,
+                                                  int32_t* __restrict__ status) {
+  __shared__ int ws[FT / 32];
+  const int64_t tile = blockIdx.x;
+  int cnt = 0;
+  bool bad = false;
+  int64_t seg = -1, sbeg = 0, send = 0;
+  double sc = 0.0;
+#pragma unroll
+  for (int k = 0; k < FPT; ++k) {
+    const int64_t e = tile * FTILE + k * FT + threadIdx.x;
+    if (e < ntot) {
+      if (seg < 0 || e >= send) {
+        seg = seg_of(off, nseg, e);
+        sbeg = off[seg];
+        send = off[seg + 1];
+        sc = scale[seg];
+      }
+      T x;
+      cnt += fin_point<T, KIND>(src, t, e, sbeg, send, sc, &x, &bad);
+    }
+  }
+  if (bad) atomicOr(status, 1);
+  int tot;
+  block_exclusive_sum<FT>(cnt, ws, &tot);
+  if (threadIdx.x == 0) tsum[tile] = tot;
+}
+
+template <typename T, int KIND>
+__global__ void __launch_bounds__(FT, 6) k_fin_write(const void* __restrict__ src,
+                                                  const T* __restrict__ t,
+                                                  const int64_t* __restrict__ off, int64_t nseg,
+                                                  const double* __restrict__ scale, int64_t ntot,
+                                                  const int64_t* __restrict__ tbase,
+                                                  T* __restrict__ t_out, T* __restrict__ v_out,
+                                                  int64_t* __restrict__ off_out) {
+  constexpr int NW = FT / 32;
+  __shared__ int s_cnt[FPT * NW];
+  __shared__ int s_tot;
+  __shared__ T s_t[FTILE], s_v[FTILE];
+  const int64_t tile = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T val[FPT];
+  uint32_t keep = 0, start = 0, ball[FPT];
+  int64_t sstart[FPT];
+  bool bad = false;
+  int64_t seg = -1, sbeg = 0, send = 0;
+  double sc = 0.0;
+#pragma unroll
+  for (int k = 0; k < FPT; ++k) {
+    const int64_t e = tile * FTILE + k * FT + threadIdx.x;
+    bool kp = false;
+    if (e < ntot) {
+      if (seg < 0 || e >= send) {
+        seg = seg_of(off, nseg, e);
+        sbeg = off[seg];
+        send = off[seg + 1];
+        sc = scale[seg];
+      }
+      kp = fin_point<T, KIND>(src, t, e, sbeg, send, sc, &val[k], &bad);
+      if (sbeg == e) {  // e starts node seg (and every empty node just before it)
+        start |= 1u << k;
+        sstart[k] = seg;
+      }
+    }
+    ball[k] = __ballot_sync(0xffffffffu, kp);
+    keep |= (uint32_t)kp << k;
+    if (lane == 0) s_cnt[k * NW + w] = __popc(ball[k]);
+  }
+  __syncthreads();
+  if (w == 0) {  // exclusive scan of the FPT * NW warp counts in point order
+    int run = 0;
+    for (int base = 0; base < FPT * NW; base += 32) {
+      const int x = base + lane < FPT * NW ? s_cnt[base + lane] : 0;
+      int inc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (base + lane < FPT * NW) s_cnt[base + lane] = run + inc - x;
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) s_tot = run;
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < FPT; ++k) {
+    const int64_t e = tile * FTILE + k * FT + threadIdx.x;
+    const int r = s_cnt[k * NW + w] + __popc(ball[k] & lt);
+    if ((keep >> k) & 1u) {
+      s_t[r] = t[e];
+      s_v[r] = val[k];
+    }
+    // a node starting at point e: its output offset is the kept count before e
+    if ((start >> k) & 1u)
+      for (int64_t q = sstart[k]; q >= 0 && off[q] == e; --q) off_out[q] = tbase[tile] + r;
+  }
+  const int tot = s_tot;
+  if (tile == gridDim.x - 1 && threadIdx.x == 0)  // the end, and nodes that start there
+    for (int64_t q = nseg; q >= 0 && off[q] >= ntot; --q) off_out[q] = tbase[tile] + tot;
+  __syncthreads();
+  const int64_t ob = tbase[tile];
+  for (int x = threadIdx.x; x < tot; x += FT) {
+    t_out[ob + x] = s_t[x];
+    v_out[ob + x] = s_v[x];
+  }
+}
+
+// single-CTA exclusive scan of n int64 counts -> out[0..n]
+__global__ void __launch_bounds__(1024) k_scan_counts(const int64_t* __restrict__ in, int64_t n,
+                                                      int64_t* __restrict__ out) {
+  __shared__ int64_t wsum[32];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b = min((int64_t)tid * per, n), e = min(b + per, n);
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += in[i];
+  int64_t x = s;
+  const int lane = tid & 31, w = tid >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t z = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z;
+  }
+  __syncthreads();
+  int64_t run = x - s + (w > 0 ? wsum[w - 1] : 0);
+  for (int64_t i = b; i < e; ++i) {
+    out[i] = run;
+    run += in[i];
+  }
+  if (tid == 1023) out[n] = run;
+}
+
+// flag counts per tile of FTILE points (for pcf_compact)
+__global__ void __launch_bounds__(FT) k_flag_count(const int32_t* __restrict__ flag,
+                                                   int64_t ntot, int64_t* __restrict__ tsum) {
+  __shared__ int ws[FT / 32];
+  const int64_t e0 = blockIdx.x * (int64_t)FTILE + threadIdx.x * FPT;
+  int c = 0;
+  for (int q = 0; q < FPT; ++q)
+    if (e0 + q < ntot) c += flag[e0 + q] != 0;
+  int tot;
+  block_exclusive_sum<FT>(c, ws, &tot);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+}
+
+// positions of the flagged points (exclusive scan within the tile + the tile base)
+__global__ void __launch_bounds__(FT) k_flag_pos(const int32_t* __restrict__ flag, int64_t ntot,
+                                                 const int64_t* __restrict__ tbase,
+                                                 int64_t* __restrict__ pos) {
+  __shared__ int ws[FT / 32];
+  const int64_t e0 = blockIdx.x * (int64_t)FTILE + threadIdx.x * FPT;
+  int c = 0;
+  for (int q = 0; q < FPT; ++q)
+    if (e0 + q < ntot) c += flag[e0 + q] != 0;
+  int tot;
+  int64_t p = tbase[blockIdx.x] + block_exclusive_sum<FT>(c, ws, &tot);
+  for (int q = 0; q < FPT; ++q)
+    if (e0 + q < ntot) {
+      pos[e0 + q] = p;
+      p += flag[e0 + q] != 0;
+    }
+}
 
 static int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
@@ -157,11 +380,8 @@ using namespace pcfb;
 extern "C" {
 
 int pcf_scan_workspace(int64_t ntot, int64_t* bytes) {
-  size_t b = 0;
-  cub::TransformInputIterator<int64_t, Widen, const int32_t*> it(nullptr, Widen());
-  cub::DeviceScan::ExclusiveSum(nullptr, b, it, (int64_t*)nullptr,
-                                (int64_t)(ntot > 0 ? ntot : 1));
-  *bytes = (int64_t)b;
+  const int64_t nt = (ntot > 0 ? ntot : 1) / FTILE + 1;
+  *bytes = 2 * (nt + 1) * (int64_t)sizeof(int64_t);
   return PCF_OK;
 }
 
@@ -174,13 +394,19 @@ int pcf_compact(int is_f32, const void* st_dev, const void* sv_dev, const void* 
                 int64_t* off_out_dev, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (ntot > 0) {
-    size_t tb = (size_t)temp_bytes;
-    cub::TransformInputIterator<int64_t, Widen, const int32_t*> it(flag_dev, Widen());
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp_dev, tb, it, pos_dev, (int64_t)ntot, s);
-    if (e != cudaSuccess) {
-      set_error("pcf_compact scan: %s", cudaGetErrorString(e));
-      return PCF_ERR_CUDA;
+    int64_t need = 0;
+    pcf_scan_workspace(ntot, &need);
+    if (!temp_dev || temp_bytes < need) {
+      set_error("pcf_compact: workspace %lld < %lld bytes", (long long)temp_bytes,
+                (long long)need);
+      return PCF_ERR_ARG;
     }
+    const int64_t nt = (ntot + FTILE - 1) / FTILE;
+    int64_t* tsum = (int64_t*)temp_dev;
+    int64_t* tbase = tsum + (nt + 1);
+    k_flag_count<<<(unsigned)nt, FT, 0, s>>>(flag_dev, ntot, tsum);
+    k_scan_counts<<<1, 1024, 0, s>>>(tsum, nt, tbase);
+    k_flag_pos<<<(unsigned)nt, FT, 0, s>>>(flag_dev, ntot, tbase, pos_dev);
     const int g = grid_for(ntot, 256);
     if (is_f32 && value_bytes == 4)
       k_scatter<float, float><<<g, 256, 0, s>>>((const float*)st_dev, (const float*)sv_dev,
@@ -247,6 +473,65 @@ int pcf_std_flag(int is_f32, int take_sqrt, const double* m2_dev, const void* t_
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("pcf_std_flag: %s", cudaGetErrorString(e));
+    return PCF_ERR_CUDA;
+  }
+  return PCF_OK;
+}
+
+
+int pcf_finalize_workspace(int64_t ntot, int64_t* bytes) {
+  if (!bytes || ntot < 0) {
+    set_error("pcf_finalize_workspace: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  const int64_t nt = (ntot > 0 ? ntot : 1) / FTILE + 1;
+  *bytes = 2 * (nt + 1) * (int64_t)sizeof(int64_t);
+  return PCF_OK;
+}
+
+int pcf_finalize(int kind, int is_f32, const void* src_dev, const void* t_dev,
+                 const int64_t* off_dev, int64_t nseg, const double* scale_dev, int64_t ntot,
+                 void* t_out_dev, void* v_out_dev, int64_t* off_out_dev, int32_t* status_dev,
+                 void* ws_dev, int64_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (kind < 0 || kind > 2 || nseg < 1 || ntot < 0 || !src_dev || !off_dev || !scale_dev ||
+      !t_out_dev || !v_out_dev || !off_out_dev || !status_dev) {
+    set_error("pcf_finalize: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  if (ntot == 0) {
+    cudaError_t e = cudaMemsetAsync(off_out_dev, 0, (nseg + 1) * sizeof(int64_t), s);
+    return e == cudaSuccess ? PCF_OK : (set_error("pcf_finalize: %s", cudaGetErrorString(e)), PCF_ERR_CUDA);
+  }
+  int64_t need = 0;
+  pcf_finalize_workspace(ntot, &need);
+  if (!ws_dev || ws_bytes < need) {
+    set_error("pcf_finalize: workspace %lld < %lld bytes", (long long)ws_bytes, (long long)need);
+    return PCF_ERR_ARG;
+  }
+  const int64_t nt = (ntot + FTILE - 1) / FTILE;
+  int64_t* tsum = (int64_t*)ws_dev;
+  int64_t* tbase = tsum + (nt + 1);
+#define PCF_FIN(T, KD)                                                                        \
+  do {                                                                                        \
+    cudaFuncSetAttribute(k_fin_write<T, KD>, cudaFuncAttributePreferredSharedMemoryCarveout,   \
+                         cudaSharedmemCarveoutMaxShared);                                     \
+    k_fin_count<T, KD><<<(unsigned)nt, FT, 0, s>>>(src_dev, (const T*)t_dev, off_dev, nseg,   \
+                                                   scale_dev, ntot, tsum, status_dev);       \
+    k_scan_counts<<<1, 1024, 0, s>>>(tsum, nt, tbase);                                        \
+    k_fin_write<T, KD><<<(unsigned)nt, FT, 0, s>>>(src_dev, (const T*)t_dev, off_dev, nseg,   \
+                                                   scale_dev, ntot, tbase, (T*)t_out_dev,    \
+                                                   (T*)v_out_dev, off_out_dev);              \
+  } while (0)
+  if (is_f32) {
+    if (kind == 0) PCF_FIN(float, 0); else if (kind == 1) PCF_FIN(float, 1); else PCF_FIN(float, 2);
+  } else {
+    if (kind == 0) PCF_FIN(double, 0); else if (kind == 1) PCF_FIN(double, 1); else PCF_FIN(double, 2);
+  }
+#undef PCF_FIN
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("pcf_finalize: %s", cudaGetErrorString(e));
     return PCF_ERR_CUDA;
   }
   return PCF_OK;

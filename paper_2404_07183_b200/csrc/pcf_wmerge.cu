@@ -28,6 +28,7 @@
 // not bound the other children's counts) is cut further inside the CTA by keys from its
 // largest contributor (halving it each time) and processed as consecutive sub-windows,
 // so any input -- including long runs of equal times -- is handled.
+#include <type_traits>
 #include "pcf_common.cuh"
 #include "pcf_internal.h"
 

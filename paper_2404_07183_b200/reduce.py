@@ -120,17 +120,6 @@ def _pairing(seg_nodes):
     return src, cnt, nxt
 
 
-class _Scratch:
-    def __init__(self, torch, n, dev, tdtype, vdtypes):
-        self.st = torch.empty(max(n, 1), dtype=tdtype, device=dev)
-        self.sv = [torch.empty(max(n, 1), dtype=d, device=dev) for d in vdtypes]
-        self.flag = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        self.pos = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
-        nb = _native.c_i64(0)
-        _native.load().pcf_scan_workspace(n, _native.ctypes.byref(nb))
-        self.temp = torch.empty(max(nb.value, 16), dtype=torch.uint8, device=dev)
-
-
 def _check_status(status, what):
     if int(status.item()) != 0:
         raise errors.NonFinite(f"{what} produced a non-finite value")
@@ -355,43 +344,30 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
 
 
 def _finalize(level: DeviceLevel, scales, kind, take_sqrt=False):
-    """kind 'scale': T(v * T(scale)) + minimise; kind 'm2': T(M2*scale) [sqrt] + minimise."""
+    """kind 'scale': T(v * T(scale)) + minimise; kind 'm2': T(M2*scale) [sqrt] + minimise.
+    One pcf_finalize call (two tiled passes; zero-width pieces dropped first)."""
     torch = _torch()
     lib = _native.load()
     dev = level.t.device
     st = current_stream_handle()
     n = level.ntot
     tdt = torch.float32 if level.is_f32 else torch.float64
-    sv = torch.empty(max(n, 1), dtype=tdt, device=dev)
-    flag = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     sc = torch.tensor(np.asarray(scales, dtype=np.float64), device=dev)
-    if kind == "scale":
-        _native.check(lib.pcf_scale_flag(int(level.is_f32), _native.ptr(level.v),
-                                         _native.ptr(level.t),
-                                         _native.ptr(level.off), level.nnodes, _native.ptr(sc), n,
-                                         _native.ptr(sv), _native.ptr(flag), _native.ptr(status),
-                                         st), "pcf_scale_flag")
-    else:
-        _native.check(lib.pcf_std_flag(int(level.is_f32), int(take_sqrt), _native.ptr(level.m2),
-                                       _native.ptr(level.t), _native.ptr(level.off),
-                                       level.nnodes, _native.ptr(sc), n,
-                                       _native.ptr(sv), _native.ptr(flag), _native.ptr(status),
-                                       st), "pcf_std_flag")
-    _check_status(status, "scaling")
-    src = torch.arange(level.nnodes, dtype=torch.int64, device=dev)
-    pos = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     nb = _native.c_i64(0)
-    lib.pcf_scan_workspace(n, _native.ctypes.byref(nb))
-    temp = torch.empty(max(nb.value, 16), dtype=torch.uint8, device=dev)
-    t_out = torch.empty_like(level.t)
+    lib.pcf_finalize_workspace(n, _native.ctypes.byref(nb))
+    ws = _scratch("fin", max(nb.value, 16), torch.uint8, dev)
+    t_out = torch.empty(max(n, 1), dtype=level.t.dtype, device=dev)
     v_out = torch.empty(max(n, 1), dtype=tdt, device=dev)
     off_out = torch.empty(level.nnodes + 1, dtype=torch.int64, device=dev)
-    _native.check(lib.pcf_compact(
-        int(level.is_f32), _native.ptr(level.t), _native.ptr(sv), None,
-        4 if level.is_f32 else 8, _native.ptr(flag), n, _native.ptr(level.off), _native.ptr(src),
-        level.nnodes, _native.ptr(pos), _native.ptr(temp), temp.numel(), _native.ptr(t_out),
-        _native.ptr(v_out), None, _native.ptr(off_out), st), "pcf_compact")
+    code = 0 if kind == "scale" else (2 if take_sqrt else 1)
+    src = level.v if kind == "scale" else level.m2
+    _native.check(lib.pcf_finalize(code, int(level.is_f32), _native.ptr(src), _native.ptr(level.t),
+                                   _native.ptr(level.off), level.nnodes, _native.ptr(sc), n,
+                                   _native.ptr(t_out), _native.ptr(v_out), _native.ptr(off_out),
+                                   _native.ptr(status), _native.ptr(ws), ws.numel(), st),
+                  "pcf_finalize")
+    _check_status(status, "scaling")
     return DeviceLevel(t_out, v_out, off_out, level.nnodes, int(off_out[-1].item()),
                        level.is_f32)
 
