@@ -9,6 +9,7 @@ ran so the log shows which kernels were covered:
   K1g k_fill_tiles_global (exact plan, rows too long to stage)
   K3  k_pack_sorted(32), diagonal, pair list
   K5  k_level_tiled (compacting level), K5m k_merge_level, moments tree, finalisers
+  K5w k_wmerge (fused levels: ties, overflowing tiles cut into sub-windows), k_fin_*
 
 usage: python tools/sanitize_cases.py [case ...]   (default: all)
 """
@@ -77,7 +78,28 @@ def case_reduce():
     print("[reduce max/mul] ok", flush=True)
 
 
-CASES = {"k1": case_k1, "k1s": case_k1s, "tail": case_tail, "reduce": case_reduce}
+def case_fused():
+    os.environ["PCF_TREE_MODE"] = "merge"
+    os.environ["PCF_TREE_FUSE"] = "4"
+    rng = np.random.default_rng(5)
+    mats = []
+    for k in range(48):  # different time scales: tiles overflow and split in the CTA
+        n = 1200 if k % 2 else 150
+        scale = 1e-3 if k % 4 == 1 else 1e3
+        tt = np.concatenate(([0.0], np.sort(rng.uniform(0, scale, n - 1))))
+        mats.append(np.column_stack((tt, rng.normal(size=n))))
+    fs = [pb.make_pcf(m) for m in mats]
+    m = pb.mean(fs)
+    s = pb.std(fs)
+    g = [pb.make_pcf(np.column_stack((np.arange(6.0), np.arange(6.0) % 4))) for _ in range(40)]
+    pb.tree_reduce(g, max)  # grid times: ties at every level
+    os.environ.pop("PCF_TREE_MODE", None)
+    os.environ.pop("PCF_TREE_FUSE", None)
+    print(f"[K5w fused] mean {m.size} pts, std {s.size} pts, ties ok", flush=True)
+
+
+CASES = {"k1": case_k1, "k1s": case_k1s, "tail": case_tail, "reduce": case_reduce,
+         "fused": case_fused}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
