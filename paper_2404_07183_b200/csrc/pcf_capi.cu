@@ -128,7 +128,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   std::vector<pcf_work_item> runs[5];  // by kernel: K1 (mode 1), K1c (3), K1s (4), K1r (2), K1g (0)
   int64_t need_max = 0, k1r_need = 0, k1c_need = 0, k1s_need = 0;
   // K1s prefetch rings at the top of shared memory, 1 KB aligned
-  const int64_t k1s_ring = (int64_t)kK1sRingSlots * kTileThreads * RB + 1024;
+  const int64_t k1s_ring = (int64_t)kK1sRingSlots * kK1sThreads * RB + 1024;
   const int64_t n_groups = (M + GW - 1) / GW;
   // K1c (one long row resident, interleaved column groups streamed): the best config for a
   // column range starting at group ks -- largest CG (fewest segments) that fits, double

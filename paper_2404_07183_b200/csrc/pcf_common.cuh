@@ -145,9 +145,11 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 // ------------------------------------------------- per-thread async copies (LDGSTS)
 // One record global -> shared, completion tracked by the issuing thread's commit groups.
 // 16-byte records bypass L1 (.cg); 8-byte records must use .ca.
-template <int BYTES>
+template <int BYTES, bool L1 = false>
 __device__ __forceinline__ void cp_async_rec(uint32_t dst, const void* src) {
-  if constexpr (BYTES == 16) {
+  if constexpr (BYTES == 16 && L1) {  // cached in L1: the rest of the 128-byte line is reused
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  } else if constexpr (BYTES == 16) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
   } else if constexpr (BYTES == 8) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");

@@ -10,6 +10,7 @@ constexpr int kTileThreads = 512;  // CTA size of the persistent tile kernels
 // K1s column prefetch ring: slots per lane (pcf_tiles.cuh kRingSlots); the ring takes
 // kRingSlots * kTileThreads records at the top of the dynamic shared memory
 constexpr int kK1sRingSlots = 8;
+constexpr int kK1sThreads = 640;  // K1s CTA size (pcf_tiles.cuh kRingThreads)
 
 typedef pcf_work_item PcfWorkItem;
 

@@ -401,7 +401,8 @@ int pcf_jit_fill_tiles(void* module, int smem_mode, const void* recs_dev, const 
     void* args[] = {&recs_dev, &recsg_dev, &soff_dev, &goff_dev, &perm_dev, &items_dev, &n_,
                     &counter_dev, &p, &a, &b, &apply, &out_dev, &ld_, &M_, &err_dev, &null_tag,
                     &null_done};
-    r = g_drv.launch(fn, grid, 1, 1, 512, 1, 1, smem, (CUstream)stream, args, nullptr);
+    const unsigned nthr = kern == 4 ? (unsigned)kK1sThreads : 512u;  // K1s: 20 warps
+    r = g_drv.launch(fn, grid, 1, 1, nthr, 1, 1, smem, (CUstream)stream, args, nullptr);
   } else {
     void* args[] = {&recs_dev, &soff_dev, &perm_dev, &items_dev, &n_, &counter_dev, &p, &a, &b,
                     &apply, &out_dev, &ld_, &M_, &err_dev, &null_tag, &null_done};

@@ -11,6 +11,7 @@
 #include "pcf_internal.h"
 #include "pcf_tiles.cuh"
 static_assert(pcfb::kRingSlots == pcfb::kK1sRingSlots, "K1s ring depth: planner and kernel disagree");
+static_assert(pcfb::kRingThreads == pcfb::kK1sThreads, "K1s CTA size: planner and kernel disagree");
 
 namespace pcfb {
 
@@ -273,7 +274,7 @@ static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
       auto kern = k_fill_rows_staged<HK, BOUNDED, OutT, Rec32, 16>;
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
       if (e != cudaSuccess) return e;
-      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+      kern<<<grid, kK1sThreads, A.smem_bytes, st>>>(
           (const Rec32*)A.recs, (const Rec32*)A.recs8, A.soff, A.goff8, A.perm, A.items,
           A.n_items, A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err,
           A.item_tag, A.tag_done);
@@ -281,7 +282,7 @@ static cudaError_t launch_tiles(const FillArgs& A, cudaStream_t st) {
       auto kern = k_fill_rows_staged<HK, BOUNDED, OutT, Rec, 8>;
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.smem_bytes);
       if (e != cudaSuccess) return e;
-      kern<<<grid, kTileThreads, A.smem_bytes, st>>>(
+      kern<<<grid, kK1sThreads, A.smem_bytes, st>>>(
           (const Rec*)A.recs, (const Rec*)A.recs8, A.soff, A.goff8, A.perm, A.items, A.n_items,
           A.counter, A.p, A.a, A.b, A.apply_root, (OutT*)A.out, A.ld, A.M, A.err, A.item_tag,
           A.tag_done);

@@ -520,6 +520,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // the last steps' requests stay in flight (~L2 latency hidden).
 constexpr int kRingSlots = 8;
 constexpr uint32_t kRingAlign = 1024;
+// K1s CTA size: 20 warps (the other tile kernels use 512 threads); 8 rows x 80 columns per
+// pass -- more warps to hide the shared-memory latency of the walk's dependent chain
+constexpr int kRingThreads = 640;
+#ifndef PCF_RING_L1
+#define PCF_RING_L1 0
+#endif
+constexpr bool kRingL1 = PCF_RING_L1;  // refills through L1 (.ca): neighbours share a line
 
 template <int HK, bool BOUNDED, typename RT>
 __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int nf,
@@ -586,7 +593,7 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
       uint32_t left, nn;  // ((x +- CS) & WRAP) | (x & ~WRAP): one LOP3 each
       asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(left) : "r"(cnext + (D - 1) * CS), "n"(WRAP), "r"(cnext));
       asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(nn) : "r"(cnext + CS), "n"(WRAP), "r"(cnext));
-      cp_async_rec<sizeof(RT)>(left, gb + boff);
+      cp_async_rec<sizeof(RT), kRingL1>(left, gb + boff);
       boff = min(boff + RB, boff_last);
       cnext = nn;
     } else {
@@ -619,7 +626,7 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
 }
 
 template <int HK, bool BOUNDED, typename OutT, typename RT, int GW>
-__global__ void __launch_bounds__(kTileThreads, 1)
+__global__ void __launch_bounds__(kRingThreads, 1)
     k_fill_rows_staged(const RT* __restrict__ recs, const RT* __restrict__ recsg,
                        const int64_t* __restrict__ soff, const int64_t* __restrict__ goff,
                        const int32_t* __restrict__ perm, const PcfWorkItem* __restrict__ items,
@@ -636,7 +643,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   // lane's slot 0
   const uint32_t ring =
       ((smem_u32(smem) + dynamic_smem_bytes() -
-        (uint32_t)(kRingSlots * kTileThreads * sizeof(RT))) & ~(kRingAlign - 1)) +
+        (uint32_t)(kRingSlots * kRingThreads * sizeof(RT))) & ~(kRingAlign - 1)) +
       (uint32_t)(tid / GW) * (kRingSlots * 128u) + (uint32_t)(tid % GW) * (uint32_t)sizeof(RT);
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -650,9 +657,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const int it = s_item;
     if (it >= n_items) break;
     const PcfWorkItem W = items[it];
-    const int logC = W.logC & 0xff;
     const int logRG = W.nrows > GW ? 1 : 0;
-    const int RG = 1 << logRG, C = 1 << logC;
+    const int RG = 1 << logRG, C = (kRingThreads / GW) >> logRG;  // columns per pass
     const int rg0 = W.row0 >> LOGGW;
     const int64_t rbase = goff[rg0];
     const uint32_t row_bytes = (uint32_t)((goff[rg0 + RG] - rbase) * sizeof(RT));
@@ -664,7 +670,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const int u = tid & (GW - 1);
     const int Q = tid >> LOGGW;
     const int rho = Q & (RG - 1);
-    const int cc = (Q >> logRG) & (C - 1);
+    const int cc = Q >> logRG;
     const int ps = W.row0 + GW * rho + u;
     const bool row_ok = ps < M;
     const RT* F = reinterpret_cast<const RT*>(smem) + (goff[rg0 + rho] - rbase) + u;
