@@ -123,12 +123,19 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
   static const bool kExactPartial = getenv("PCF_NO_EXACT_PARTIAL") == nullptr;
   static const bool kK1sEnabled = getenv("PCF_NO_K1S") == nullptr;
+  // K1r merge-path split: with the column rings one lane per pair is fastest (c4 K1r
+  // 71.8 ms at G = 1 vs 87.8 ms at G <= 32: each segment pays a co-rank search and a ring
+  // fill from L2), and it is the bitwise sum
+  static const int kK1rMaxLogG = getenv("PCF_K1R_MAXLOG2G") ? atoi(getenv("PCF_K1R_MAXLOG2G")) : 0;
   static const int kSingleFallbackLogG =
       getenv("PCF_SINGLE_FALLBACK_LOG2G") ? atoi(getenv("PCF_SINGLE_FALLBACK_LOG2G")) : -1;
   std::vector<pcf_work_item> runs[5];  // by kernel: K1 (mode 1), K1c (3), K1s (4), K1r (2), K1g (0)
   int64_t need_max = 0, k1r_need = 0, k1c_need = 0, k1s_need = 0;
   // K1s prefetch rings at the top of shared memory, 1 KB aligned
   const int64_t k1s_ring = (int64_t)kK1sRingSlots * kK1sThreads * RB + 1024;
+  // K1r: rings of the 512 lanes, 8 or 4 slots
+  const int64_t k1r_ring8 = (int64_t)kK1sRingSlots * kTileThreads * RB + 1024;
+  const int64_t k1r_ring4 = (int64_t)4 * kTileThreads * RB + 1024;
   const int64_t n_groups = (M + GW - 1) / GW;
   // K1c (one long row resident, interleaved column groups streamed): the best config for a
   // column range starting at group ks -- largest CG (fewest segments) that fits, double
@@ -242,6 +249,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     }
     const bool smem = best_logRG >= 0 && (r0 % GW) == 0;
     int rows, logC, logG, s_mode = -1;
+    bool ring4 = false;  // K1r: 4-slot column rings (flag bit 9 of logC)
     if (smem && !single && best_logG >= kSingleMinLogG) {
       // long rows: G >= 16 merge-path segments of a few dozen steps each.  A single
       // column buffer of twice the columns halves G (half the co-rank searches and
@@ -261,16 +269,25 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       rows = GW << best_logRG;
       logC = best_logC;
       logG = best_logG;
-    } else if (sizes[r0] >= kK1rMinRecs && al(sizes[r0] * RB) <= smem_budget) {
+    } else if (sizes[r0] >= kK1rMinRecs &&
+               al(sizes[r0] * RB) + k1r_ring4 <= smem_budget) {
       // K1r: this long row alone resident in shared memory, C columns x G segments per
       // pass; G keeps >= ~128 walk steps per lane (row length dominates long-row pairs).
       // Short rows that miss K1 (exact mode: G = 1 needs 64 staged columns) stay on K1g,
       // whose 32-row passes re-use each column from L1.
       rows = 1;
       logG = 0;
-      while (logG < std::min(max_log2G, 5) && (sizes[r0] >> (logG + 1)) >= 128) ++logG;
+      while (logG < std::min(std::min(max_log2G, 5), kK1rMaxLogG) &&
+             (sizes[r0] >> (logG + 1)) >= 128)
+        ++logG;
       logC = 9 - logG;
-      k1r_need = std::max(k1r_need, al(sizes[r0] * RB));
+      // the lanes' column rings (8 slots; 4 when the row leaves no room for 8: flag bit 9)
+      if (al(sizes[r0] * RB) + k1r_ring8 <= smem_budget) {
+        k1r_need = std::max(k1r_need, al(sizes[r0] * RB) + k1r_ring8);
+      } else {
+        k1r_need = std::max(k1r_need, al(sizes[r0] * RB) + k1r_ring4);
+        ring4 = true;
+      }
     } else if (max_log2G == 0 && kK1sEnabled && (r0 % GW) == 0 &&
                al(group_recs(r0) * RB) + k1s_ring <= smem_budget) {
       // K1s (exact mode): the row block staged as in K1, columns through each lane's
@@ -345,7 +362,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       w.nrows = (int32_t)Rr;
       w.col0 = (int32_t)c0;
       w.col1 = (int32_t)c1;
-      w.logC = logC | (single ? 0x100 : 0);
+      w.logC = logC | (single ? 0x100 : 0) | (ring4 ? 0x200 : 0);
       w.log2G = logG;
       w.smem_mode = mode;
       const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;

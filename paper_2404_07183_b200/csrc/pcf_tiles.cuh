@@ -528,43 +528,73 @@ constexpr int kRingThreads = 640;
 #endif
 constexpr bool kRingL1 = PCF_RING_L1;  // refills through L1 (.ca): neighbours share a line
 
-template <int HK, bool BOUNDED, typename RT>
+// The walk of one lane over merge-path segment `lane` of 2^log2G (G = 1: the whole pair,
+// left to right -- the reference's sum) with the row in shared memory (stride SF records:
+// GW for K1s's interleaved groups, 1 for K1r's contiguous row) and the column streamed
+// through the lane's ring of D slots (slot k at ring + k * 128).
+template <int HK, bool BOUNDED, typename RT, int D, int SF>
 __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int nf,
                                                  const RT* __restrict__ gcol, int ng,
-                                                 uint32_t ring, double p, double a, double b) {
+                                                 uint32_t ring, int lane, int log2G, double p,
+                                                 double a, double b) {
   using ST = decltype(RT::t);
-  constexpr int D = kRingSlots;
   constexpr uint32_t RB = (uint32_t)sizeof(RT);
-  constexpr uint32_t RS = 128;               // row record stride (GW interleaved records)
+  constexpr uint32_t RS = SF * RB;           // row record stride (bytes)
   constexpr uint32_t CS = 128;               // ring slot stride
   constexpr uint32_t WRAP = (D - 1) * CS;    // slot-index bits of a ring address
   static_assert(D * CS <= kRingAlign && (D & (D - 1)) == 0, "ring slots");
-  const int SF = 128 / (int)sizeof(RT);
   int k0 = 0, m0 = 0;
   if (a > 0.0) {  // start cursors k = max{i : t_i <= a} (pyx:33-36)
     k0 = upper_bound_count(nf - 1, a, [&](int x) { return (double)F[x * SF].t; });
     m0 = upper_bound_count(ng - 1, a, [&](int x) { return (double)gcol[x].t; });
   }
-  const int steps = (nf - 1 - k0) + (ng - 1 - m0);
+  const RT* __restrict__ Fk = F + k0 * SF;
+  const RT* __restrict__ Gm = gcol + m0;
+  const int Nf = nf - 1 - k0, Ng = ng - 1 - m0;
+  const int N = Nf + Ng;
+  const int d0 = (int)(((long long)lane * N) >> log2G);
+  const int d1 = (int)(((long long)(lane + 1) * N) >> log2G);
+  int i = 0;
+  if (log2G > 0) {  // co-rank of diagonal d0 (see lane_walk); the column from L2
+    int lo = max(0, d0 - Ng), hi = min(d0, Nf);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (Fk[mid * SF].t <= Gm[d0 - mid - 1].t) lo = mid + 1;
+      else hi = mid;
+    }
+    i = lo;
+  }
+  const int j = d0 - i;
+  double t;
+  if (d0 == 0) {
+    t = a;
+  } else {
+    const double tfp = i > 0 ? (double)Fk[(i - 1) * SF].t : 0.0;
+    const double tgp = j > 0 ? (double)Gm[j - 1].t : 0.0;
+    t = fmax(tfp, tgp);
+  }
+  if (BOUNDED) t = fmin(t, b);
+  const int steps = d1 - d0;
+  const int jc0 = m0 + j;  // the lane's first column record
   const char* gb = reinterpret_cast<const char*>(gcol);
   const uint32_t boff_last = (uint32_t)(ng - 1) * RB;
   // the previous pair's in-flight prefetches must land before their slots are reused
   cp_async_wait<0>();
 #pragma unroll
-  for (int i = 0; i < D; ++i) {
-    const uint32_t r = (uint32_t)min(m0 + i, ng - 1);
-    cp_async_rec<sizeof(RT)>(ring + (uint32_t)((m0 + i) & (D - 1)) * CS, gb + r * RB);
+  for (int x = 0; x < D; ++x) {
+    const uint32_t r = (uint32_t)min(jc0 + x, ng - 1);
+    cp_async_rec<sizeof(RT)>(ring + (uint32_t)((jc0 + x) & (D - 1)) * CS, gb + r * RB);
   }
   cp_async_commit();
   cp_async_wait<0>();
-  uint32_t boff = (uint32_t)min(m0 + D, ng - 1) * RB;      // next record to request
-  const uint32_t cslot = ring + (uint32_t)(m0 & (D - 1)) * CS;  // the current column record
+  uint32_t boff = (uint32_t)min(jc0 + D, ng - 1) * RB;    // next record to request
+  const uint32_t cslot = ring + (uint32_t)(jc0 & (D - 1)) * CS;  // the current column record
   // loop-carried: the slot of the NEXT column record.  The slot a column advance leaves
   // (refill target) is recomputed from it as a temporary, so no register an in-flight
   // LDGSTS still has to read is overwritten right after it (a WAR stall on the MIO queue)
   uint32_t cnext;
   asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(cnext) : "r"(cslot + CS), "n"(WRAP), "r"(cslot));
-  uint32_t rnext = smem_u32(F + k0 * SF);
+  uint32_t rnext = smem_u32(Fk + i * SF);
   ST tr, vr, tc, vc;
   lds_rec(rnext, tr, vr);
   lds_rec(cslot, tc, vc);
@@ -574,8 +604,6 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
   bool xc = tc < tr;
   ST tx = xc ? tc : tr, ty = xc ? tr : tc, vy = xc ? vr : vc;
   const ST vx = xc ? vc : vr;
-  double t = a;
-  if (BOUNDED) t = fmin(t, b);
   double acc = 0.0;
   double hc = hval<HK>((double)vx, (double)vy, p);
   auto step = [&]() {
@@ -609,19 +637,26 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
     xc = xc != sw;
   };
   int s = 0;
+  if constexpr (D >= 8) {
+    // one commit group per two steps: a record read at step s was requested at step
+    // <= s - (D - 1), i.e. in a group at least 3 groups old, so waiting until <= 2 groups
+    // are pending before each pair of steps covers both
 #pragma unroll 2
-  for (; s + 1 < steps; s += 2) {
-    cp_async_wait<(D - 3) / 2>();
-    step();
+    for (; s + 1 < steps; s += 2) {
+      cp_async_wait<(D - 3) / 2>();
+      step();
+      step();
+      cp_async_commit();
+    }
+  }
+#pragma unroll 2
+  for (; s < steps; ++s) {  // one group per step: requested >= D - 1 steps before
+    cp_async_wait<(D >= 8 ? (D - 3) / 2 : D - 2)>();  // (after pairs: groups of two steps)
     step();
     cp_async_commit();
   }
-  if (s < steps) {
-    cp_async_wait<(D - 3) / 2>();
-    step();
-    cp_async_commit();
-  }
-  if (BOUNDED && (HK != H_USER || b > t)) acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(b, t)));
+  if (BOUNDED && (lane == (1 << log2G) - 1) && (HK != H_USER || b > t))
+    acc = __dadd_rn(acc, __dmul_rn(hc, __dsub_rn(b, t)));
   return acc;
 }
 
@@ -687,7 +722,8 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       if (row_ok && qs < W.col1 && qs > ps) {
         const RT* Gv = recs + soff[qs];
         const int ng = (int)(soff[qs + 1] - soff[qs]);
-        const double acc = lane_walk_ring<HK, BOUNDED, RT>(F, nf, Gv, ng, ring, p, a, b);
+        const double acc =
+            lane_walk_ring<HK, BOUNDED, RT, kRingSlots, GW>(F, nf, Gv, ng, ring, 0, 0, p, a, b);
         const double hl = BOUNDED ? 0.0 : hval<HK>((double)F[(nf - 1) * GW].v,
                                                    (double)Gv[ng - 1].v, p);
         finish_entry<HK, BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
@@ -703,13 +739,12 @@ __global__ void __launch_bounds__(kRingThreads, 1)
 // K1r: row-resident tiles for rows too long for K1's 8-row groups (the heavy tail of c4).
 //
 // A work item is ONE size-sorted row x a column range.  The row is loaded into shared
-// memory once per item and re-read by every pair of the item; the (shorter) columns are
-// read through L1/L2.  For a long row against shorter columns almost every step of the
-// walk advances the row cursor, so nearly all operand traffic lands in shared memory
-// instead of costing one L1 line lookup per lane per step (K1g).  Lanes: C = 512/G
-// columns x G merge-path segments, the G lanes of a pair contiguous in one warp.  Row
-// loads from lanes at unrelated positions do conflict (random bank groups); the column
-// share of the steps goes to L1.  G = 1 (exact mode) is the reference's left-to-right
+// memory once per item and re-read by every pair of the item; the (long) columns stream
+// through each lane's prefetch ring (lane_walk_ring, as in K1s: cp.async refills kRingSlots
+// records ahead; 4 slots for the few rows too long to leave room for 8 -- item flag
+// logC bit 9).  Lanes: C = 512/G columns x G merge-path segments, the G lanes of a pair
+// contiguous in one warp.  Row loads from lanes at unrelated positions do conflict (random
+// bank groups); ring loads do not.  G = 1 (exact mode) is the reference's left-to-right
 // sum, bit for bit.
 template <int HK, bool BOUNDED, typename OutT, typename RT>
 __global__ void __launch_bounds__(kTileThreads, 1)
@@ -722,9 +757,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RT* rowS = reinterpret_cast<RT*>(smem_raw);
   __shared__ int s_item;
+  constexpr int GWL = 128 / (int)sizeof(RT);  // lanes per 128-byte ring slot row
   const int tid = threadIdx.x;
+  const uint32_t top = smem_u32(smem_raw) + dynamic_smem_bytes();
   int cur_row = -1;
   for (;;) {
+    cp_async_wait<0>();  // no ring refill may still be landing when the row is replaced
     if (tid == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();  // also: every lane is done with the previous row
     const int it = s_item;
@@ -738,7 +776,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       cur_row = ps;
     }
     __syncthreads();
-    const int C = 1 << W.logC, log2G = W.log2G;
+    const bool small_ring = (W.logC >> 9) & 1;
+    const int D = small_ring ? 4 : kRingSlots;
+    const uint32_t ring = ((top - (uint32_t)(D * kTileThreads * sizeof(RT))) & ~(kRingAlign - 1)) +
+                          (uint32_t)(tid / GWL) * (uint32_t)(D * 128) +
+                          (uint32_t)(tid % GWL) * (uint32_t)sizeof(RT);
+    const int C = 1 << (W.logC & 0xff), log2G = W.log2G;
     const int cc = tid >> log2G;
     const int lane = tid & ((1 << log2G) - 1);
     for (int cb = max(W.col0, ps + 1); cb < W.col1; cb += C) {
@@ -749,7 +792,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       int ng = 0;
       if (ok) {
         ng = (int)(soff[qs + 1] - soff[qs]);
-        acc = lane_walk<HK, BOUNDED, 1, 1, RT>(rowS, nf, Gv, ng, lane, log2G, p, a, b);
+        acc = small_ring
+                  ? lane_walk_ring<HK, BOUNDED, RT, 4, 1>(rowS, nf, Gv, ng, ring, lane, log2G,
+                                                          p, a, b)
+                  : lane_walk_ring<HK, BOUNDED, RT, kRingSlots, 1>(rowS, nf, Gv, ng, ring, lane,
+                                                                   log2G, p, a, b);
       }
       for (int o = (1 << log2G) >> 1; o >= 1; o >>= 1)
         acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));

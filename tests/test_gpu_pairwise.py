@@ -338,8 +338,9 @@ def test_streamed_long_pairs(oracle, recipe, f32, bounds):
         t, v = t.astype(np.float32), v.astype(np.float32)
     coll = DeviceCollection(t, v, off)
     M = coll.M
-    dev, host, smem = coll.plan(smem_budget=48 * 1024)
-    # long ECC rows go to K1r, App-A rows (< 1024 records) that miss K1 to K1g
+    # ECC: 80 KB leaves room for K1r's 4-slot column rings next to rows of 1024..~3000
+    # records (longer rows go to K1g); App-A rows (< 1024 records) that miss K1 go to K1g
+    dev, host, smem = coll.plan(smem_budget=(80 if recipe == "ecc" else 48) * 1024)
     assert (host[:, 6] == (2 if recipe == "ecc" else 0)).sum() > 0
     a, b = bounds
     rows = np.unique(np.linspace(0, M - 2, 10).astype(int))
