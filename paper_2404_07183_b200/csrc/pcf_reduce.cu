@@ -8,6 +8,7 @@
 // recompute and write the kept points through shared memory, coalesced), so neither the
 // scaled values nor the flags ever go to HBM.  pcf_compact (flags -> positions -> scatter)
 // uses the same tile scan.  No library scan on this path.
+#include <type_traits>
 #include "pcf_common.cuh"
 #include "pcf_internal.h"
 
@@ -159,17 +160,41 @@ __device__ __forceinline__ T fin_value(const void* __restrict__ src, int64_t q, 
 }
 
 // point e: value and keep flag (first point of its node, or a value change against the
-// last survivor; zero-width pieces dropped).  seg: the node of e (found by the caller).
+// last survivor; zero-width pieces dropped).  The warp's 32 consecutive points load their
+// own time and source value once; the neighbours' come by shuffles (one extra load at each
+// end of the warp), so a point's loads never wait for another's.
 template <typename T, int KIND>
 __device__ __forceinline__ bool fin_point(const void* __restrict__ src, const T* __restrict__ t,
-                                          int64_t e, int64_t sbeg, int64_t send, double sc,
-                                          T* val, bool* bad) {
-  const T x = fin_value<T, KIND>(src, e, sc);
+                                          int64_t e, int64_t ntot, int64_t sbeg, int64_t send,
+                                          double sc, T* val, bool* bad) {
+  using SV = typename std::conditional<KIND == 0, T, double>::type;
+  const SV* sv = reinterpret_cast<const SV*>(src);
+  const int lane = threadIdx.x & 31;
+  const bool in = e < ntot;
+  const T te = in ? t[e] : (T)0;
+  const SV xe = in ? sv[e] : (SV)0;
+  T tn = __shfl_down_sync(0xffffffffu, te, 1);
+  T tp = __shfl_up_sync(0xffffffffu, te, 1);
+  SV xp = __shfl_up_sync(0xffffffffu, xe, 1);
+  if (lane == 31 && e + 1 < ntot) tn = t[e + 1];
+  if (lane == 0 && e > 0) {
+    tp = t[e - 1];
+    xp = sv[e - 1];
+  }
+  auto value = [&](SV x) -> T {
+    if (KIND == 0) return (T)x * to_t<T>(sc);
+    const T var = to_t<T>((double)x * sc);
+    return KIND == 2 ? to_t<T>(sqrt((double)var)) : var;
+  };
+  const T x = value(xe);
   *val = x;
-  if (zero_width(t, e, send)) return false;
+  if (!in) return false;
+  if (t && e + 1 < send && tn == te) return false;  // zero-width piece
   if (!isfinite((double)x)) *bad = true;
-  const int64_t p = prev_survivor(t, e, sbeg);
-  return p < sbeg || x != fin_value<T, KIND>(src, p, sc);
+  if (e == sbeg) return true;  // first point of its node
+  if (!t || tp != te) return x != value(xp);  // the previous point is the last survivor
+  const int64_t p = prev_survivor(t, e, sbeg);  // inside a run of equal times (rare)
+  return p < sbeg || x != value(sv[p]);
 }
 
 // node of point e (largest k with off[k] <= e)
@@ -187,7 +212,7 @@ __device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ off, int64
 // A tile is FPT rows of FT consecutive points; warp w of row k handles 32 consecutive
 // points (coalesced loads), its keep flags are one ballot.  Point order = (row, warp, lane).
 template <typename T, int KIND>
-__global__ void __launch_bounds__(FT, 6) k_fin_count(const void* __restrict__ src,
+__global__ void __launch_bounds__(FT, 4) k_fin_count(const void* __restrict__ src,
                                                   const T* __restrict__ t,
                                                   const int64_t* __restrict__ off, int64_t nseg,
                                                   const double* __restrict__ scale, int64_t ntot,
@@ -202,16 +227,14 @@ __global__ void __launch_bounds__(FT, 6) k_fin_count(const void* __restrict__ sr
 #pragma unroll
   for (int k = 0; k < FPT; ++k) {
     const int64_t e = tile * FTILE + k * FT + threadIdx.x;
-    if (e < ntot) {
-      if (seg < 0 || e >= send) {
-        seg = seg_of(off, nseg, e);
-        sbeg = off[seg];
-        send = off[seg + 1];
-        sc = scale[seg];
-      }
-      T x;
-      cnt += fin_point<T, KIND>(src, t, e, sbeg, send, sc, &x, &bad);
+    if (e < ntot && (seg < 0 || e >= send)) {
+      seg = seg_of(off, nseg, e);
+      sbeg = off[seg];
+      send = off[seg + 1];
+      sc = scale[seg];
     }
+    T x;  // every lane takes part (the point's neighbours come by shuffles)
+    cnt += fin_point<T, KIND>(src, t, e, ntot, sbeg, send, sc, &x, &bad);
   }
   if (bad) atomicOr(status, 1);
   int tot;
@@ -220,7 +243,7 @@ __global__ void __launch_bounds__(FT, 6) k_fin_count(const void* __restrict__ sr
 }
 
 template <typename T, int KIND>
-__global__ void __launch_bounds__(FT, 6) k_fin_write(const void* __restrict__ src,
+__global__ void __launch_bounds__(FT, 4) k_fin_write(const void* __restrict__ src,
                                                   const T* __restrict__ t,
                                                   const int64_t* __restrict__ off, int64_t nseg,
                                                   const double* __restrict__ scale, int64_t ntot,
@@ -242,22 +265,24 @@ __global__ void __launch_bounds__(FT, 6) k_fin_write(const void* __restrict__ sr
 #pragma unroll
   for (int k = 0; k < FPT; ++k) {
     const int64_t e = tile * FTILE + k * FT + threadIdx.x;
-    bool kp = false;
-    if (e < ntot) {
-      if (seg < 0 || e >= send) {
-        seg = seg_of(off, nseg, e);
-        sbeg = off[seg];
-        send = off[seg + 1];
-        sc = scale[seg];
-      }
-      kp = fin_point<T, KIND>(src, t, e, sbeg, send, sc, &val[k], &bad);
-      if (sbeg == e) {  // e starts node seg (and every empty node just before it)
-        start |= 1u << k;
-        sstart[k] = seg;
-      }
+    if (e < ntot && (seg < 0 || e >= send)) {
+      seg = seg_of(off, nseg, e);
+      sbeg = off[seg];
+      send = off[seg + 1];
+      sc = scale[seg];
     }
-    ball[k] = __ballot_sync(0xffffffffu, kp);
+    const bool kp = fin_point<T, KIND>(src, t, e, ntot, sbeg, send, sc, &val[k], &bad);
+    if (e < ntot && sbeg == e) {  // e starts node seg (and every empty node just before it)
+      start |= 1u << k;
+      sstart[k] = seg;
+    }
     keep |= (uint32_t)kp << k;
+  }
+  // ballots after all the points' loads are in flight (a ballot per point would make every
+  // point's loads wait for the previous point's)
+#pragma unroll
+  for (int k = 0; k < FPT; ++k) {
+    ball[k] = __ballot_sync(0xffffffffu, (keep >> k) & 1u);
     if (lane == 0) s_cnt[k * NW + w] = __popc(ball[k]);
   }
   __syncthreads();
@@ -494,7 +519,7 @@ int pcf_finalize(int kind, int is_f32, const void* src_dev, const void* t_dev,
                  void* t_out_dev, void* v_out_dev, int64_t* off_out_dev, int32_t* status_dev,
                  void* ws_dev, int64_t ws_bytes, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (kind < 0 || kind > 2 || nseg < 1 || ntot < 0 || !src_dev || !off_dev || !scale_dev ||
+  if (kind < 0 || kind > 2 || nseg < 1 || ntot < 0 || !src_dev || !t_dev || !off_dev || !scale_dev ||
       !t_out_dev || !v_out_dev || !off_out_dev || !status_dev) {
     set_error("pcf_finalize: bad arguments");
     return PCF_ERR_ARG;
