@@ -311,6 +311,11 @@ int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v
                           const int64_t* leaves_dev, int64_t nout, int32_t nlev, int64_t ntot,
                           void* t_out_dev, void* v_out_dev, double* v2_out_dev,
                           int64_t* off_out_dev, void* ws_dev, int64_t ws_bytes, void* stream);
+/* Equal-time coincidences between neighbouring nodes (2p, 2p+1) of a level, over nsample
+ * pairs spread across it: counts[0] = coincidences, counts[1] = points examined.  Lets the
+ * host run a tree non-compacting from level 0 when breakpoints are nearly distinct. */
+int pcf_tree_dup_sample(int is_f32, const void* t_dev, const int64_t* off_dev, int64_t nnodes,
+                        int32_t nsample, unsigned long long* counts_dev, void* stream);
 /* Whole finalisation of a reduction tree's root level(s) in two tiled passes (no flag or
  * scaled-value arrays in HBM): kind 0 = mean, v * T(scale[seg]) (core.scale + the final
  * minimize_discretization, reduce.py:211-217); kind 1 = variance T(M2 * scale[seg]);

@@ -114,6 +114,7 @@ SIGNATURES = {
     "pcf_tree_merge_level": (
         c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
                 c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pcf_tree_dup_sample": (c_int, [c_int, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pcf_finalize_workspace": (c_int, [c_i64, c_i64p]),
     "pcf_finalize": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp,
                              c_vp, c_vp, c_vp, c_i64, c_vp]),

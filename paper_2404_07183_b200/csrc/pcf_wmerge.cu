@@ -608,6 +608,30 @@ __global__ void __launch_bounds__(WTH, 3)
   }
 }
 
+// Equal-time coincidences between neighbouring nodes (2p, 2p+1) for nsample pairs spread
+// over the level: counts[0] += coincidences, counts[1] += points.  Decides before level 0
+// whether the tree can run non-compacting (nearly distinct breakpoints) from the start.
+template <typename T>
+__global__ void k_dup_sample(const T* __restrict__ t, const int64_t* __restrict__ off,
+                             int64_t nnodes, int nsample, unsigned long long* __restrict__ counts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsample || nnodes < 2) return;
+  const int64_t pa = 2 * ((int64_t)i * (nnodes / 2) / nsample);
+  const T* a = t + off[pa];
+  const T* b = t + off[pa + 1];
+  const int64_t na = off[pa + 1] - off[pa], nb = off[pa + 2] - off[pa + 1];
+  int64_t x = 0, y = 0;
+  unsigned long long dup = 0;
+  while (x < na && y < nb) {
+    const T u = a[x], w = b[y];
+    dup += (u == w);
+    x += (u <= w);
+    y += (w <= u);
+  }
+  atomicAdd(&counts[0], dup);
+  atomicAdd(&counts[1], (unsigned long long)(na + nb));
+}
+
 }  // namespace wm
 }  // namespace pcfb
 
@@ -703,6 +727,30 @@ int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("pcf_tree_merge_levels: %s", cudaGetErrorString(e));
+    return PCF_ERR_CUDA;
+  }
+  return PCF_OK;
+}
+
+int pcf_tree_dup_sample(int is_f32, const void* t_dev, const int64_t* off_dev, int64_t nnodes,
+                        int32_t nsample, unsigned long long* counts_dev, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!t_dev || !off_dev || !counts_dev || nnodes < 0 || nsample < 1) {
+    set_error("pcf_tree_dup_sample: bad arguments");
+    return PCF_ERR_ARG;
+  }
+  cudaError_t e = cudaMemsetAsync(counts_dev, 0, 2 * sizeof(unsigned long long), s);
+  if (e == cudaSuccess && nnodes >= 2) {
+    const int g = (nsample + 127) / 128;
+    if (is_f32)
+      k_dup_sample<float><<<g, 128, 0, s>>>((const float*)t_dev, off_dev, nnodes, nsample, counts_dev);
+    else
+      k_dup_sample<double><<<g, 128, 0, s>>>((const double*)t_dev, off_dev, nnodes, nsample,
+                                             counts_dev);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    set_error("pcf_tree_dup_sample: %s", cudaGetErrorString(e));
     return PCF_ERR_CUDA;
   }
   return PCF_OK;

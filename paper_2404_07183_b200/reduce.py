@@ -279,11 +279,24 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
     fuse = max(1, min(4, int(fuse_env))) if fuse_env else (1 if moments else 4)
     pkey = (None if leaves0 is not None or np.asarray(seg_nodes).size > 64 else
             (tuple(int(x) for x in np.asarray(seg_nodes)), bool(moments), str(dev)))
+    merge0 = False  # level 0 too runs non-compacting (fused with the levels above it)
+    if mode == "auto" and fuse > 1 and len(plan) > 1 and level.nnodes >= 2:
+        # a sample of neighbouring leaf pairs: nearly distinct breakpoints mean compaction
+        # would drop (almost) nothing, so every level can be a fused merge
+        counts = _scratch("dup", 2, torch.int64, dev)
+        _native.check(lib.pcf_tree_dup_sample(int(level.is_f32), _native.ptr(cur_t),
+                                              _native.ptr(cur_off), level.nnodes,
+                                              min(4096, level.nnodes // 2), _native.ptr(counts),
+                                              st), "pcf_tree_dup_sample")
+        dup, seen = (int(x) for x in counts.cpu())
+        merge0 = merge = seen > 0 and dup <= 0.02 * seen
+    elif mode == "merge" and fuse > 1:
+        merge0 = True
     li = 0
     nbuf = 0
     while li < len(plan):
         src, cnt, _ = plan[li]
-        if merge and li > 0 and fuse > 1 and len(plan) - li > 1:
+        if merge and (li > 0 or merge0) and fuse > 1 and len(plan) - li > 1:
             # several non-compacting levels in one pass (pcf_tree_merge_levels, K5w)
             g = min(fuse, len(plan) - li)
             nfirst, ncnt = _fused_tables(plan, li, li + g, pkey, dev)
@@ -325,7 +338,7 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
         else:
             _native.check(lib.pcf_tree_level(kind, *args, _native.ptr(status), st),
                           "pcf_tree_level")
-        if li == 0 and len(plan) > 1 and mode == "auto":
+        if li == 0 and len(plan) > 1 and mode == "auto" and not merge0:
             # nearly distinct breakpoints (compaction kept >= 90% of level 0): the upper
             # levels would drop almost nothing, so they run without compaction
             kept = int(off_out[-1].item())

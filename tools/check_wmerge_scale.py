@@ -12,8 +12,9 @@ for M in [3000, 10000, 30000, 60000, 100000]:
     res = {}
     for fz in ("1", "4"):
         os.environ["PCF_TREE_FUSE"] = fz
-        out, _ = R._run_tree(lvl, [M], op=0)
-        res[fz] = (out.t[:out.ntot].cpu().numpy().copy(), out.v[:out.ntot].cpu().numpy().copy())
+        out = R.mean_packed(lvl)  # finalised: fused and level-by-level trees differ only in
+        res[fz] = (out.t[:out.ntot].cpu().numpy().copy(),  # which zero-width pieces exist
+                   out.v[:out.ntot].cpu().numpy().copy())
     a, b = res["1"], res["4"]
     d = np.flatnonzero(a[0] != b[0])
     print(M, "same t", np.array_equal(a[0], b[0]), "same v", np.array_equal(a[1], b[1]),
