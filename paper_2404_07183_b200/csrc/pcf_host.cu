@@ -24,11 +24,16 @@
 // allocator); pcf_release_workspace() frees it.
 #include <dlfcn.h>
 #include <stdio.h>
+#include <sys/mman.h>
 #include <stdlib.h>
 #include <string.h>
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
 #include <mutex>
+#include <thread>
+#include <memory>
 #include <numeric>
 #include <vector>
 #include "pcf_internal.h"
@@ -108,6 +113,140 @@ cudaError_t copy_rows(const std::vector<int32_t>& perm, const std::vector<int32_
   }
   return cudaSuccess;
 }
+
+// ---- result in pageable host memory (e.g. the numpy array pdist returns): pinning an
+// 80 GB result costs ~56 s on the GPU box (1.4 GB/s), so the finished rows go through a
+// small pinned staging pool instead -- D2H into a slot, host worker threads copy the slot's
+// rows to their places (transparent huge pages requested for the result), slot reused.
+struct PinnedPool {
+  char* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedPool() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t get(size_t n, char** out) {
+    if (bytes < n) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      bytes = 0;
+      cudaError_t e = cudaHostAlloc((void**)&p, n, cudaHostAllocDefault);
+      if (e != cudaSuccess) return e;
+      bytes = n;
+    }
+    *out = p;
+    return cudaSuccess;
+  }
+};
+PinnedPool g_pin;
+
+class Stager {
+ public:
+  Stager(char* out, int64_t M, int64_t ld, size_t es, const char* d_out, char* pool, int nslot,
+         size_t slot_rows)
+      : out_(out), M_(M), ld_(ld), es_(es), d_out_(d_out), nslot_(nslot), slot_rows_(slot_rows) {
+    const size_t row = (size_t)M * es;
+    for (int k = 0; k < nslot; ++k) {
+      slot_.push_back(pool + (size_t)k * slot_rows * row);
+      cudaEvent_t ev = nullptr;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      ev_.push_back(ev);
+      free_.push_back(k);
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nw = (int)std::max(2u, std::min(16u, hw ? hw / 2 : 4u));
+    for (int w = 0; w < nw; ++w) workers_.emplace_back([this] { work(); });
+  }
+  ~Stager() { finish(); }
+  // D2H of the given original rows (ascending) on stream st, through the slots
+  cudaError_t drain(const std::vector<int64_t>& rows, cudaStream_t st) {
+    const size_t row = (size_t)M_ * es_;
+    for (size_t k0 = 0; k0 < rows.size(); k0 += slot_rows_) {
+      const size_t k1 = std::min(rows.size(), k0 + slot_rows_);
+      int slot;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return !free_.empty() || err_; });
+        if (err_) return cudaErrorUnknown;
+        slot = free_.front();
+        free_.pop_front();
+      }
+      for (size_t k = k0; k < k1;) {  // runs of consecutive rows: one copy each
+        size_t e = k + 1;
+        while (e < k1 && rows[e] == rows[e - 1] + 1) ++e;
+        const cudaError_t rc =
+            cudaMemcpyAsync(slot_[slot] + (k - k0) * row, d_out_ + (size_t)rows[k] * row,
+                            row * (e - k), cudaMemcpyDeviceToHost, st);
+        if (rc != cudaSuccess) return rc;
+        k = e;
+      }
+      cudaError_t rc = cudaEventRecord(ev_[slot], st);
+      if (rc != cudaSuccess) return rc;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        q_.push_back(Piece{slot, std::vector<int64_t>(rows.begin() + k0, rows.begin() + k1)});
+      }
+      cv_.notify_all();
+    }
+    return cudaSuccess;
+  }
+  // wait for every queued row to reach the result; returns false on a CUDA error
+  bool finish() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      done_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+    workers_.clear();
+    for (auto ev : ev_)
+      if (ev) cudaEventDestroy(ev);
+    ev_.clear();
+    return !err_;
+  }
+
+ private:
+  struct Piece {
+    int slot;
+    std::vector<int64_t> rows;
+  };
+  void work() {
+    const size_t row = (size_t)M_ * es_;
+    for (;;) {
+      Piece pc;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return !q_.empty() || done_; });
+        if (q_.empty()) return;
+        pc = std::move(q_.front());
+        q_.pop_front();
+      }
+      const bool ok = cudaEventSynchronize(ev_[pc.slot]) == cudaSuccess;
+      if (ok)
+        for (size_t k = 0; k < pc.rows.size(); ++k)
+          memcpy(out_ + (size_t)pc.rows[k] * (size_t)ld_ * es_, slot_[pc.slot] + k * row, row);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!ok) err_ = true;
+        free_.push_back(pc.slot);
+      }
+      cv_.notify_all();
+    }
+  }
+  char* out_;
+  int64_t M_, ld_;
+  size_t es_;
+  const char* d_out_;
+  int nslot_;
+  size_t slot_rows_;
+  std::vector<char*> slot_;
+  std::vector<cudaEvent_t> ev_;
+  std::deque<int> free_;
+  std::deque<Piece> q_;
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool done_ = false, err_ = false;
+};
 
 // cuStreamWaitValue32 from the driver (opened at run time; null if unavailable): lets the
 // copy stream wait on the fill kernel's per-chunk completion counters, so the whole
@@ -244,7 +383,11 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
            (double)(w.col1 - w.col0) * rows_pts;
   };
   static const bool row_order = getenv("PCF_HOST_ROW_ORDER") != nullptr;  // A/B timing
+  // kernel-major (one persistent launch per kernel), then the sweep within each kernel
+  auto mode_rank = [](int m) { return m == 1 ? 0 : (m == 3 ? 1 : (m == 4 ? 2 : (m == 2 ? 3 : 4))); };
   std::stable_sort(items.begin(), items.end(), [&](const pcf_work_item& x, const pcf_work_item& y) {
+    const int mx = mode_rank(x.smem_mode), my = mode_rank(y.smem_mode);
+    if (mx != my) return mx < my;
     if (row_order) return x.row0 < y.row0;
     if (x.col0 != y.col0) return x.col0 > y.col0;
     return x.cost_hi > y.cost_hi;
@@ -299,7 +442,6 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
     for (int64_t x = 0; x < M; ++x) chunk_rows[owner[x] < 0 ? 0 : owner[x]].push_back((int32_t)x);
   }
   // inside a chunk: one run per kernel (K1, K1c, K1s, K1r, K1g), each longest-first
-  auto mode_rank = [](int m) { return m == 1 ? 0 : (m == 3 ? 1 : (m == 4 ? 2 : (m == 2 ? 3 : 4))); };
   for (auto& ch : chunks) {
     std::stable_sort(items.begin() + ch.i0, items.begin() + ch.i1,
                      [&](const pcf_work_item& x, const pcf_work_item& y) {
@@ -386,14 +528,39 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   }
   std::vector<cudaEvent_t> evs(chunks.size(), nullptr);
   int status = PCF_OK;
-  bool one_mode = n_items > 0;
-  for (int64_t i = 1; i < n_items && one_mode; ++i)
-    one_mode = items[i].smem_mode == items[0].smem_mode;
+  // result in pinned memory: rows go straight to it; pageable: through the staging pool
+  cudaPointerAttributes pattr;
+  const bool pinned_out = cudaPointerGetAttributes(&pattr, out) == cudaSuccess &&
+                          pattr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  std::unique_ptr<Stager> stager;
+  if (!pinned_out) {
+    const size_t row = (size_t)M * es;
+    const size_t slot_rows = std::max<size_t>(1, std::min<size_t>((size_t)M, (128u << 20) / row));
+    const int nslot = 8;
+    char* pool = nullptr;
+    if ((e = g_pin.get((size_t)nslot * slot_rows * row, &pool)))
+      return cudaStreamSynchronize(s0), fail(e, "pcf_matrix_host staging pool");
+    {  // transparent huge pages for the result: 512x fewer first-touch page faults
+      const uintptr_t b = ((uintptr_t)out + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+      const uintptr_t en = ((uintptr_t)out + (size_t)M * (size_t)ld * es) & ~(uintptr_t)((2u << 20) - 1);
+      if (en > b) madvise((void*)b, en - b, MADV_HUGEPAGE);
+    }
+    stager.reset(new Stager((char*)out, M, ld, es, (const char*)d_out, pool, nslot, slot_rows));
+  }
+  auto drain = [&](size_t k, cudaStream_t sc) -> cudaError_t {
+    if (!stager) return copy_rows(perm, chunk_rows[k], (const char*)d_out, (char*)out, M, ld, es, sc);
+    std::vector<int64_t> o(chunk_rows[k].size());
+    for (size_t x = 0; x < o.size(); ++x) o[x] = perm[chunk_rows[k][x]];
+    std::sort(o.begin(), o.end());
+    return stager->drain(o, sc);
+  };
   const WaitValue32 wait = stream_wait_fn();
   bool single = false;
-  if (one_mode && wait) {
-    // ONE persistent launch over the row-block-ordered queue; item i bumps
-    // done[chunk(i)]; the copy stream waits for each chunk's count, then drains its rows
+  if (n_items > 0 && wait) {
+    // ONE persistent launch per kernel over its run of the queue (kernel-major order);
+    // item i bumps done[chunk(i)]; the copy streams wait for each chunk's count, then
+    // drain its rows
     std::vector<int32_t> tag(n_items);
     for (size_t k = 0; k < chunks.size(); ++k)
       for (int64_t i = chunks[k].i0; i < chunks[k].i1; ++i) tag[i] = (int32_t)k;
@@ -408,14 +575,19 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
         (e = cudaStreamWaitEvent(s2, zeroed, 0)))
       return fail(e, "pcf_matrix_host single-launch setup");
     evs[0] = zeroed;  // destroyed with the others
-    A.items = (const PcfWorkItem*)d_items;
-    A.n_items = (int)n_items;
-    A.smem_mode = items[0].smem_mode;
-    A.item_tag = (const int32_t*)d_tag;
     A.tag_done = (int32_t*)d_done;
     if (timing) cudaEventRecord(tev[1], s0);
-    if ((e = cudaMemsetAsync(d_cnt, 0, 4, s0)) || (e = launch_fill_tiles(A, s0)))
-      return fail(e, "pcf_matrix_host fill");
+    for (int64_t i = 0; i < n_items;) {
+      int64_t j = i;
+      while (j < n_items && items[j].smem_mode == items[i].smem_mode) ++j;
+      A.items = (const PcfWorkItem*)d_items + i;
+      A.n_items = (int)(j - i);
+      A.smem_mode = items[i].smem_mode;
+      A.item_tag = (const int32_t*)d_tag + i;
+      if ((e = cudaMemsetAsync(d_cnt, 0, 4, s0)) || (e = launch_fill_tiles(A, s0)))
+        return fail(e, "pcf_matrix_host fill");
+      i = j;
+    }
     if (timing) cudaEventRecord(tev[2], s0);
     single = true;
     for (size_t k = 0; k < chunks.size() && status == PCF_OK; ++k) {
@@ -432,7 +604,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
         }
       }
       if (status) break;
-      if ((e = copy_rows(perm, chunk_rows[k], (const char*)d_out, (char*)out, M, ld, es, sc))) {
+      if ((e = drain(k, sc))) {
         status = fail(e, "pcf_matrix_host drain");
         break;
       }
@@ -455,7 +627,7 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
     if (status) break;
     if ((e = cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming)) ||
         (e = cudaEventRecord(evs[k], s0)) || (e = cudaStreamWaitEvent(s1, evs[k], 0)) ||
-        (e = copy_rows(perm, chunk_rows[k], (const char*)d_out, (char*)out, M, ld, es, s1))) {
+        (e = drain(k, s1))) {
       status = fail(e, "pcf_matrix_host drain");
       break;
     }
@@ -475,6 +647,8 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
     cudaStreamSynchronize(s1);
     cudaStreamSynchronize(s2);
   }
+  if (stager && !stager->finish() && status == PCF_OK)
+    status = fail(cudaErrorUnknown, "pcf_matrix_host staged drain");
   for (auto ev : evs)
     if (ev) cudaEventDestroy(ev);
   if (timing) {

@@ -183,10 +183,10 @@ class MatrixJob:
         torch = require_cuda()
         tcat, vcat, off = pack_matrices([f.to_matrix() for f in self._coll], self._dtype)
         M = int(off.shape[0] - 1)
-        # pinned (page-locked) result from torch's caching host allocator, so the row
-        # copies overlap the fill; the returned array keeps the buffer alive
-        tdt = torch.float32 if self._dtype == np.float32 else torch.float64
-        out = torch.empty((M, M), dtype=tdt, pin_memory=True).numpy()
+        # pageable result (pinning an 80 GB array costs about a minute): finished rows go
+        # through pcf_matrix_host's small pinned staging pool, copied into place by host
+        # threads while the fill continues
+        out = np.empty((M, M), dtype=np.float32 if self._dtype == np.float32 else np.float64)
         out, bad = matrix_host(tcat, vcat, off, self._op, self._p, self._apply_root,
                                self._diag, self._a, self._b, exact=exact, out=out)
         if bad is not None:

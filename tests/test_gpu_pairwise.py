@@ -444,3 +444,25 @@ def test_all_tile_kernels_against_oracle(oracle, f32, exact, bounds):
                 assert np.array_equal(got, want), i
             else:
                 assert rel_err(got, want) < TOL64, i
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_matrix_host_pinned_and_pageable_results_agree(exact):
+    """pcf_matrix_host writes a pinned result directly and a pageable one through its
+    pinned staging pool (host threads copy the rows into place); both, and a strided
+    (ld > M) pageable result, hold the same bits."""
+    import torch
+
+    from paper_2404_07183_b200.engine import matrix_host
+
+    t, v, off = dg.synthetic_benchmark_packed(900, rng=pb.RngSpec(17))
+    M = len(off) - 1
+    pinned = torch.empty((M, M), dtype=torch.float64, pin_memory=True).numpy()
+    a, bad_a = matrix_host(t, v, off, 0, 1.0, True, False, exact=exact, out=pinned)
+    b, bad_b = matrix_host(t, v, off, 0, 1.0, True, False, exact=exact,
+                           out=np.empty((M, M)))
+    wide = np.full((M, M + 37), -1.0)
+    c, bad_c = matrix_host(t, v, off, 0, 1.0, True, False, exact=exact, out=wide[:, :M])
+    assert bad_a is None and bad_b is None and bad_c is None
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert (wide[:, M:] == -1.0).all()  # the padding columns untouched
