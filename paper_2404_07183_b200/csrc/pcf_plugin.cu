@@ -19,6 +19,7 @@
 // so fill_block == integrate_pair bit for bit as in the reference
 // (tests/test_matrix.py:41-47); max_log2G > 0 selects the fast plan.
 #include <math.h>
+#include <sys/mman.h>
 #include <stdlib.h>
 #include <string.h>
 #include <algorithm>
@@ -360,6 +361,13 @@ int pcf_collection_fill_block(void* handle, int64_t r0, int64_t r1, int op, doub
     } else {
       m = C->mat;
     }
+  }
+  {  // transparent huge pages for the (usually fresh, np.zeros) result: the row and mirror
+     // writes below are its first touch, and 2 MB pages fault 512x less often
+    const size_t es = out_is_f32 ? 4 : 8;
+    const uintptr_t b0 = ((uintptr_t)out + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+    const uintptr_t b1 = ((uintptr_t)out + (size_t)M * (size_t)ld * es) & ~(uintptr_t)((2u << 20) - 1);
+    if (r0 == 0 && b1 > b0) madvise((void*)b0, b1 - b0, MADV_HUGEPAGE);
   }
   // rows [r0, r1), columns [c0, M): c0 = the block's first column that is written
   const int64_t c0 = diag ? r0 : std::min(r0 + 1, M);
