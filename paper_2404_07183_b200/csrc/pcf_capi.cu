@@ -123,6 +123,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
   static const bool kExactPartial = getenv("PCF_NO_EXACT_PARTIAL") == nullptr;
   static const bool kK1sEnabled = getenv("PCF_NO_K1S") == nullptr;
+  static const int kFastRingMinLogG =
+      getenv("PCF_FAST_RING_MINLOG2G") ? atoi(getenv("PCF_FAST_RING_MINLOG2G")) : -1;
   // K1r merge-path split: with the column rings one lane per pair is fastest (c4 K1r
   // 71.8 ms at G = 1 vs 87.8 ms at G <= 32: each segment pays a co-rank search and a ring
   // fill from L2), and it is the bitwise sum
@@ -247,7 +249,12 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
         }
       }
     }
-    const bool smem = best_logRG >= 0 && (r0 % GW) == 0;
+    bool smem = best_logRG >= 0 && (r0 % GW) == 0;
+    // fast plan, long rows: K1 would split each pair into >= 2^kFastRingMinLogG merge-path
+    // segments; K1s (one lane per pair, columns through prefetch rings) instead
+    const bool use_ring = smem && kFastRingMinLogG >= 0 && best_logG >= kFastRingMinLogG &&
+                          kK1sEnabled && al(group_recs(r0) * RB) + k1s_ring <= smem_budget;
+    if (use_ring) smem = false;
     int rows, logC, logG, s_mode = -1;
     bool ring4 = false;  // K1r: 4-slot column rings (flag bit 9 of logC)
     if (smem && !single && best_logG >= kSingleMinLogG) {
@@ -288,7 +295,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
         k1r_need = std::max(k1r_need, al(sizes[r0] * RB) + k1r_ring4);
         ring4 = true;
       }
-    } else if (max_log2G == 0 && kK1sEnabled && (r0 % GW) == 0 &&
+    } else if ((max_log2G == 0 || use_ring) && kK1sEnabled && (r0 % GW) == 0 &&
                al(group_recs(r0) * RB) + k1s_ring <= smem_budget) {
       // K1s (exact mode): the row block staged as in K1, columns through each lane's
       // prefetch ring, 64 quarters = RG x C columns per pass
