@@ -28,6 +28,7 @@
 // not bound the other children's counts) is cut further inside the CTA by keys from its
 // largest contributor (halving it each time) and processed as consecutive sub-windows,
 // so any input -- including long runs of equal times -- is handled.
+#include <string.h>
 #include <type_traits>
 #include "pcf_common.cuh"
 #include "pcf_internal.h"
@@ -38,6 +39,7 @@ namespace wm {
 constexpr int WTH = 256;   // threads per tile CTA
 constexpr int WLPT = 8;    // merge positions per thread per round
 constexpr int KMAXC = 16;  // children per output node (k <= 4 levels per pass)
+constexpr int kTreeTgt = 512;  // points per K5t tile (one thread each)
 enum { K_ADD = 0, K_MAX = 1, K_MIN = 2, K_MUL = 3, K_MOM = 4 };
 
 template <int K>
@@ -79,9 +81,8 @@ __device__ __forceinline__ int key_lower(const T* __restrict__ tc, int c, double
 }
 
 // per output node: tile count (>= 1) from its point count
-template <typename T, int K>
 __global__ void k_wnodes(const int64_t* __restrict__ off, const int64_t* __restrict__ nfirst,
-                         const int32_t* __restrict__ ncnt, int64_t nout,
+                         const int32_t* __restrict__ ncnt, int64_t nout, int64_t tgt,
                          int64_t* __restrict__ tcount, int64_t* __restrict__ off_out) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q <= nout;
        q += (int64_t)gridDim.x * blockDim.x) {
@@ -92,7 +93,7 @@ __global__ void k_wnodes(const int64_t* __restrict__ off, const int64_t* __restr
     const int64_t f = nfirst[q];
     const int64_t n = off[f + ncnt[q]] - off[f];
     off_out[q] = off[f];
-    tcount[q] = n > 0 ? (n + Cfg<T, K>::TGT - 1) / Cfg<T, K>::TGT : 1;
+    tcount[q] = n > 0 ? (n + tgt - 1) / tgt : 1;
   }
 }
 
@@ -608,6 +609,140 @@ __global__ void __launch_bounds__(WTH, 3)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K5t: the same fused levels as a streaming merge tree per THREAD.  One thread owns one
+// tile (the key-ordered window of an output node, same tiles as K5w) and pulls its points
+// in order through a static binary tree of 2-way mergers held in registers: a merger keeps
+// the next point of each input (time + value) and each input's current value; next() takes
+// the input whose next point comes first (A on ties), refills it from below and returns
+// (t, combine(cur_A, cur_B)) -- a passthrough merger (empty right subtree) returns cur_A.
+// The leaves read their child's points from global memory.  No shared memory, barriers or
+// co-rank searches: ~D compares and D combines per output point for D levels.  Measured
+// slower than K5w (each thread streams 2^D lists from global memory, uncoalesced; 186
+// registers at D = 3), so it is opt-in: PCF_TREE_KERNEL=tree.
+template <typename T, int K, int D>
+struct MNode {
+  MNode<T, K, D - 1> a, b;
+  T ta, tb;       // next point times of a and b (+inf when exhausted)
+  T va, vb;       // values of those next points
+  T ca, cb;       // current values of a and b
+  bool hasb;      // right subtree holds at least one child
+  __device__ __forceinline__ void init(const T* __restrict__ t, const T* __restrict__ v,
+                                       const int64_t* cbase, const int* lo, const int* en,
+                                       int C, int first, T* carry) {
+    hasb = first + (1 << (D - 1)) < C;
+    T cra, crb;
+    a.init(t, v, cbase, lo, en, C, first, &cra);
+    b.init(t, v, cbase, lo, en, C, first + (1 << (D - 1)), &crb);
+    ca = cra;
+    cb = crb;
+    *carry = hasb ? to_t<T>(vop<K>((double)cra, (double)crb)) : cra;
+    a.next(ta, va);
+    b.next(tb, vb);
+  }
+  __device__ __forceinline__ void next(T& t, T& v) {
+    if (ta <= tb) {  // A first on ties
+      t = ta;
+      ca = va;
+      a.next(ta, va);
+    } else {
+      t = tb;
+      cb = vb;
+      b.next(tb, vb);
+    }
+    v = hasb ? to_t<T>(vop<K>((double)ca, (double)cb)) : ca;
+  }
+};
+
+template <typename T, int K>
+struct MNode<T, K, 0> {  // one child of the output node: its window [pos, end) in global
+  const T* __restrict__ tp;
+  const T* __restrict__ vp;
+  int pos, end;
+  __device__ __forceinline__ void init(const T* __restrict__ t, const T* __restrict__ v,
+                                       const int64_t* cbase, const int* lo, const int* en,
+                                       int C, int first, T* carry) {
+    if (first < C) {
+      tp = t + cbase[first];
+      vp = v + cbase[first];
+      pos = lo[first];
+      end = en[first];
+      *carry = vp[pos > 0 ? pos - 1 : 0];  // reduce_pair's t = 0 convention at pos 0
+    } else {  // no such child
+      tp = t;
+      vp = v;
+      pos = end = 0;
+      *carry = (T)0;
+    }
+  }
+  __device__ __forceinline__ void next(T& t, T& v) {
+    if (pos < end) {
+      t = tp[pos];
+      v = vp[pos];
+      ++pos;
+    } else {
+      t = (T)INFINITY;
+      v = (T)0;
+    }
+  }
+};
+
+template <typename T, int K, int D>
+__global__ void __launch_bounds__(128)
+    k_wtree(const T* __restrict__ t, const T* __restrict__ v, int64_t nout,
+            const int64_t* __restrict__ tbase, const TileHead* __restrict__ th,
+            const TileChild* __restrict__ tc, T* __restrict__ t_out, T* __restrict__ v_out) {
+  const int64_t ntiles = tbase[nout];
+  for (int64_t tl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tl < ntiles;
+       tl += (int64_t)gridDim.x * blockDim.x) {
+    const TileHead h = th[tl];
+    const int C = h.C;
+    int64_t cbase[1 << D];
+    int lo[1 << D], en[1 << D];
+    int64_t count = 0, before = 0;
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+      if (c < C) {
+        const TileChild e = tc[tl * KMAXC + c];
+        cbase[c] = e.cb;
+        lo[c] = e.lo;
+        en[c] = e.end;
+        count += e.end - e.lo;
+        before += e.lo;
+      } else {
+        cbase[c] = 0;
+        lo[c] = en[c] = 0;
+      }
+    }
+    MNode<T, K, D> root;
+    T carry;
+    root.init(t, v, cbase, lo, en, C, 0, &carry);
+    const int64_t ob = cbase[0] + before;  // node start (first child's start) + points before
+    for (int64_t o = 0; o < count; ++o) {
+      T tt, vv;
+      root.next(tt, vv);
+      t_out[ob + o] = tt;
+      v_out[ob + o] = vv;
+    }
+  }
+}
+
+template <typename T, int K>
+void launch_tree(int nlev, const T* t, const T* v, int64_t nout, const int64_t* tbase,
+                 const TileHead* th, const TileChild* tc, T* t_out, T* v_out, int64_t ntile_max,
+                 int nsm, cudaStream_t s) {
+  if constexpr (K != K_MOM) {
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((ntile_max + 127) / 128, (int64_t)nsm * 32));
+    if (nlev == 1)
+      k_wtree<T, K, 1><<<grid, 128, 0, s>>>(t, v, nout, tbase, th, tc, t_out, v_out);
+    else if (nlev == 2)
+      k_wtree<T, K, 2><<<grid, 128, 0, s>>>(t, v, nout, tbase, th, tc, t_out, v_out);
+    else
+      k_wtree<T, K, 3><<<grid, 128, 0, s>>>(t, v, nout, tbase, th, tc, t_out, v_out);
+  }
+}
+
 // Equal-time coincidences between neighbouring nodes (2p, 2p+1) for nsample pairs spread
 // over the level: counts[0] += coincidences, counts[1] += points.  Decides before level 0
 // whether the tree can run non-compacting (nearly distinct breakpoints) from the start.
@@ -647,8 +782,8 @@ int pcf_tree_merge_levels_workspace(int64_t ntot, int64_t nout, int64_t* bytes) 
     set_error("pcf_tree_merge_levels_workspace: bad arguments");
     return PCF_ERR_ARG;
   }
-  const int64_t nb = ntot / 1024 + 2 * nout + 2;
-  const int64_t nt = ntot / 1024 + nout + 1;  // tiles (upper bound)
+  const int64_t nb = ntot / kTreeTgt + 2 * nout + 2;
+  const int64_t nt = ntot / kTreeTgt + nout + 1;  // tiles (upper bound)
   *bytes = 2 * (nout + 1) * 8 + nb * KMAXC * 4 + nout * KMAXC * 4 + nt * 16 +
            nt * KMAXC * 16 + 512;
   return PCF_OK;
@@ -679,8 +814,8 @@ int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v
   int64_t* tbase = tcount + (nout + 1);
   int32_t* rr = (int32_t*)(tbase + (nout + 1));
   int32_t* rb = rr + nout * KMAXC;
-  const int64_t ntile_max = ntot / 1024 + nout + 1;
-  uintptr_t pth = (uintptr_t)(rb + (ntot / 1024 + 2 * nout + 2) * KMAXC);
+  const int64_t ntile_max = ntot / kTreeTgt + nout + 1;
+  uintptr_t pth = (uintptr_t)(rb + (ntot / kTreeTgt + 2 * nout + 2) * KMAXC);
   pth = (pth + 15) & ~(uintptr_t)15;
   TileHead* th = (TileHead*)pth;
   TileChild* tch = (TileChild*)(th + ntile_max);
@@ -690,21 +825,32 @@ int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v
   int nsm = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // K5t is opt-in (PCF_TREE_KERNEL=tree): bit-identical, but each thread's eight
+  // uncoalesced input streams make it 2.4-3.2x slower than K5w on c5 (40-54 vs 16.7 ms)
+  static const bool tree_env = getenv("PCF_TREE_KERNEL") != nullptr &&
+                               strcmp(getenv("PCF_TREE_KERNEL"), "tree") == 0;
+  const bool tree = tree_env && kind != K_MOM && nlev <= 3;  // K5t (per-thread merge tree)
 #define PCF_WM(T, K)                                                                          \
   do {                                                                                        \
-    k_wnodes<T, K><<<ng, 256, 0, s>>>(off_dev, nfirst_dev, ncnt_dev, nout, tcount,             \
-                                      off_out_dev);                                           \
+    k_wnodes<<<ng, 256, 0, s>>>(off_dev, nfirst_dev, ncnt_dev, nout,                          \
+                                tree ? (int64_t)kTreeTgt : (int64_t)Cfg<T, K>::TGT, tcount,    \
+                                off_out_dev);                                                 \
     k_scan1<<<1, 1024, 0, s>>>(tcount, nout, tbase);                                          \
     k_wruns<T><<<rg, 256, 0, s>>>((const T*)t_dev, off_dev, nfirst_dev, ncnt_dev, nout, rr);  \
     k_wbounds<T, K><<<bg, 256, 0, s>>>((const T*)t_dev, off_dev, nfirst_dev, ncnt_dev, nout,  \
                                        tbase, rr, rb);                                        \
     k_wtiles<<<bg, 256, 0, s>>>(off_dev, nfirst_dev, ncnt_dev, tbase, rb, nout, th, tch);     \
-    const int dsm = Cfg<T, K>::SMEM;                                                          \
-    cudaFuncSetAttribute(k_wmerge<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);   \
-    const int64_t grid = std::min<int64_t>(ntot / Cfg<T, K>::TGT + nout + 1, 3 * nsm);        \
-    k_wmerge<T, K><<<(unsigned)grid, WTH, dsm, s>>>(                                          \
-        (const T*)t_dev, v_dev, v2_dev, off_dev, nfirst_dev, ncnt_dev, leaves_dev, nout, nlev, \
-        tbase, th, tch, (T*)t_out_dev, v_out_dev, v2_out_dev);                                \
+    if (tree && K != K_MOM) {                                                                 \
+      launch_tree<T, K>(nlev, (const T*)t_dev, (const T*)v_dev, nout, tbase, th, tch,          \
+                        (T*)t_out_dev, (T*)v_out_dev, ntile_max, nsm, s);                     \
+    } else {                                                                                  \
+      const int dsm = Cfg<T, K>::SMEM;                                                        \
+      cudaFuncSetAttribute(k_wmerge<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm); \
+      const int64_t grid = std::min<int64_t>(ntot / Cfg<T, K>::TGT + nout + 1, 3 * nsm);      \
+      k_wmerge<T, K><<<(unsigned)grid, WTH, dsm, s>>>(                                        \
+          (const T*)t_dev, v_dev, v2_dev, off_dev, nfirst_dev, ncnt_dev, leaves_dev, nout,    \
+          nlev, tbase, th, tch, (T*)t_out_dev, v_out_dev, v2_out_dev);                        \
+    }                                                                                         \
   } while (0)
   if (is_f32) {
     switch (kind) {

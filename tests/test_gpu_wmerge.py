@@ -107,3 +107,18 @@ def test_float32_and_fibres(monkeypatch):
     for a, b in zip(ref, got):
         assert np.array_equal(a[:, 0], b[:, 0])
         assert np.max(np.abs(a[:, 1] - b[:, 1]) / np.maximum(np.abs(a[:, 1]), 1e-30)) < 1e-6
+
+
+def test_thread_tree_kernel_matches(monkeypatch):
+    """K5t (PCF_TREE_KERNEL=tree: one thread per tile, a register merge tree) gives the
+    same bits as the shared-memory fused kernel and the level-by-level path."""
+    _, mats = dg.noisy_trig_matrices((2000,), 60, "sin", 0.1, dg.RngSpec(21))
+    fs = [pb.make_pcf(m) for m in mats]
+    monkeypatch.setenv("PCF_TREE_FUSE", "1")
+    ref = pb.mean(fs).to_matrix()
+    monkeypatch.setenv("PCF_TREE_KERNEL", "tree")
+    for fz in ("2", "3"):
+        monkeypatch.setenv("PCF_TREE_FUSE", fz)
+        assert np.array_equal(pb.mean(fs).to_matrix(), ref)
+        assert np.array_equal(pb.tree_reduce(fs, max).to_matrix(),
+                              pb.tree_reduce(fs[:], max).to_matrix())
