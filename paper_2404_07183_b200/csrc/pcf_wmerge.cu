@@ -36,7 +36,7 @@
 namespace pcfb {
 namespace wm {
 
-constexpr int WTH = 256;   // threads per tile CTA
+constexpr int WTH = 256;   // threads per tile CTA (192, or 128 with 1024-point tiles, and 2048-point tiles at 2 CTAs/SM all measured slower)
 constexpr int WLPT = 8;    // merge positions per thread per round
 constexpr int KMAXC = 16;  // children per output node (k <= 4 levels per pass)
 constexpr int kTreeTgt = 512;  // points per K5t tile (one thread each)
@@ -846,7 +846,10 @@ int pcf_tree_merge_levels(int kind, int is_f32, const void* t_dev, const void* v
     } else {                                                                                  \
       const int dsm = Cfg<T, K>::SMEM;                                                        \
       cudaFuncSetAttribute(k_wmerge<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm); \
-      const int64_t grid = std::min<int64_t>(ntot / Cfg<T, K>::TGT + nout + 1, 3 * nsm);      \
+      int per_sm = 0;                                                                         \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wmerge<T, K>, WTH, dsm);        \
+      const int64_t grid =                                                                    \
+          std::min<int64_t>(ntot / Cfg<T, K>::TGT + nout + 1, (int64_t)std::max(1, per_sm) * nsm); \
       k_wmerge<T, K><<<(unsigned)grid, WTH, dsm, s>>>(                                        \
           (const T*)t_dev, v_dev, v2_dev, off_dev, nfirst_dev, ncnt_dev, leaves_dev, nout,    \
           nlev, tbase, th, tch, (T*)t_out_dev, v_out_dev, v2_out_dev);                        \
