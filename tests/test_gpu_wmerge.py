@@ -122,3 +122,20 @@ def test_thread_tree_kernel_matches(monkeypatch):
         assert np.array_equal(pb.mean(fs).to_matrix(), ref)
         assert np.array_equal(pb.tree_reduce(fs, max).to_matrix(),
                               pb.tree_reduce(fs[:], max).to_matrix())
+
+
+@pytest.mark.parametrize("mode", ["auto", "compact", "merge"])
+def test_overflow_is_nonfinite_in_every_tree_mode(monkeypatch, mode):
+    """A sum that overflows raises NonFinite like reduce_pair does (reduce.py:49-53),
+    whether the levels compact, merge one by one or run fused."""
+    from paper_2404_07183_b200 import errors
+
+    monkeypatch.setenv("PCF_TREE_MODE", mode)
+    rng = np.random.default_rng(2)
+    fs = []
+    for _ in range(64):
+        tt = np.concatenate(([0.0], np.sort(rng.uniform(0, 1, 9))))
+        fs.append(pb.make_pcf(np.column_stack((tt, np.full(10, 1.0e307)))))
+    with pytest.raises(errors.NonFinite):
+        pb.tree_reduce(fs, "add")
+    assert np.isfinite(pb.tree_reduce(fs, max).to_matrix()[:, 1]).all()
