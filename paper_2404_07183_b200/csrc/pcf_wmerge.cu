@@ -277,37 +277,6 @@ __global__ void k_wbounds(const T* __restrict__ t, const int64_t* __restrict__ o
 
 __device__ __forceinline__ int pad(int x) { return x + (x >> 3); }  // WLPT = 8
 
-// merge state of output list l at local position m: its A / B input spans and co-ranks
-struct ListPos {
-  int a0, na, b0, nb, i, j;
-  bool pass;
-};
-
-template <typename T>
-__device__ __forceinline__ ListPos open_list(const int* ls, int nl, int l, int m,
-                                             const T* it) {
-  ListPos L;
-  L.a0 = ls[2 * l];
-  L.pass = 2 * l + 1 >= nl;
-  L.na = ls[2 * l + 1] - L.a0;  // a passthrough list ends at ls[nl]
-  L.b0 = ls[2 * l + 1];
-  L.nb = L.pass ? 0 : ls[2 * l + 2] - L.b0;
-  if (L.pass) {
-    L.i = m;
-    L.j = 0;
-    return L;
-  }
-  int lo = max(0, m - L.nb), hi = min(m, L.na);
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (it[pad(L.a0 + mid)] <= it[pad(L.b0 + m - mid - 1)]) lo = mid + 1;
-    else hi = mid;
-  }
-  L.i = lo;
-  L.j = m - lo;
-  return L;
-}
-
 template <typename T, int K>
 __global__ void __launch_bounds__(WTH, 3)
     k_wmerge(const T* __restrict__ t, const void* __restrict__ v_, const double* __restrict__ v2,
@@ -334,11 +303,10 @@ __global__ void __launch_bounds__(WTH, 3)
   };
   __shared__ int64_t s_cb[KMAXC];                 // first input position of each child
   __shared__ int s_lo[KMAXC], s_hi[KMAXC], s_end[KMAXC];
-  __shared__ int s_ls[2][KMAXC + 1];              // list spans (ping-pong with the levels)
-  __shared__ VT s_cv[2][KMAXC];                   // carries
-  __shared__ double s_c2[2][KMAXC];
-  __shared__ double s_lv[2][KMAXC];               // leaf counts (moments weights)
-  __shared__ double s_w[2][KMAXC / 2][2];         // per output list: nB / n, nA * nB / n
+  __shared__ int s_ls[2][KMAXC + 1];              // s_ls[0]: children spans in the buffers
+  __shared__ VT s_cv[5][KMAXC];                   // carries per level and list (0: children)
+  __shared__ double s_c2[5][KMAXC];
+  __shared__ double s_lv[5][KMAXC];               // leaf counts (moments weights)
   __shared__ int s_tot, s_big, s_ki;
   __shared__ double s_kt;
   __shared__ int64_t s_wbase;
@@ -412,176 +380,170 @@ __global__ void __launch_bounds__(WTH, 3)
       s_ls[0][C] = run;
       s_wbase = wb;
     }
-    if (tid < C) {  // carries: the child's point before the window (its first point at 0)
-      const int64_t pc = s_cb[tid] + (s_lo[tid] > 0 ? s_lo[tid] - 1 : 0);
-      cp_async_rec<sizeof(VT)>(smem_u32(&s_cv[0][tid]), v + pc);
-      if (MOM) cp_async_rec<8>(smem_u32(&s_c2[0][tid]), v2 + pc);
-    }
     __syncthreads();
-    // ---- stage the children's ranges, concatenated in child order (coalesced per child);
-    //      shared layout: element x at x + x / WLPT (one pad slot per thread's run, so the
-    //      runs of WLPT consecutive elements the threads write fall in distinct banks)
+    // ---- the k levels, warp groups per list: at level L (1..D, D = ceil(log2 C)) output
+    //      list i holds children [i 2^L, (i+1) 2^L) and is merged by warps
+    //      [i g, (i+1) g), g = 8 >> (D - L); those warps produced its two inputs at level
+    //      L - 1 (or staged its children), so they sync among themselves only (named
+    //      barriers) -- one CTA barrier per tile instead of one per level
+    const int D = C > 1 ? 32 - __clz(C - 1) : 0;  // levels that combine anything
+    const int warp = tid >> 5, lane = tid & 31;
+    auto group_sync = [&](int gsz, int grp) {
+      if (gsz == 1) {
+        __syncwarp();
+      } else if (gsz == WTH / 32) {
+        __syncthreads();
+      } else {  // ids 1..4 for pairs of warps, 5..6 for quads
+        const int id = (gsz == 2 ? 1 : 5) + grp;
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(gsz * 32) : "memory");
+      }
+    };
     {
+      // staging: the level-1 group of list j stages children 2j, 2j + 1 (and their carries)
+      const int g1 = D > 0 ? (WTH / 32) >> (D - 1) : WTH / 32;
+      const int grp = warp / g1, r = tid - grp * g1 * 32;
       T* st = bt(0);
       VT* sv = bv(0);
       double* s2 = b2(0);
-      // warp w copies children w, w + 8, ...: no per-element child lookup; asynchronous
-      // copies keep every load of the tile in flight at once
-      const int lane = tid & 31;
-      for (int c = tid >> 5; c < C; c += WTH / 32) {
+      const int c0 = D > 0 ? 2 * grp : 0, c1 = D > 0 ? min(2 * grp + 2, C) : C;
+      for (int c = c0; c < c1; ++c) {
         const int x0 = s_ls[0][c], x1 = s_ls[0][c + 1];
         const T* gt = t + (s_cb[c] + s_lo[c] - x0);
         const VT* gv = v + (s_cb[c] + s_lo[c] - x0);
         const double* g2 = v2 + (s_cb[c] + s_lo[c] - x0);
-        for (int x = x0 + lane; x < x1; x += 32) {
+        for (int x = x0 + r; x < x1; x += g1 * 32) {
           const int y = pad(x);
           cp_async_rec<sizeof(T)>(smem_u32(st + y), gt + x);
           cp_async_rec<sizeof(VT)>(smem_u32(sv + y), gv + x);
           if (MOM) cp_async_rec<8>(smem_u32(s2 + y), g2 + x);
         }
+        if (r == 0) {  // the child's point before the window (its first point at 0)
+          const int64_t pc = s_cb[c] + (s_lo[c] > 0 ? s_lo[c] - 1 : 0);
+          cp_async_rec<sizeof(VT)>(smem_u32(&s_cv[0][c]), v + pc);
+          if (MOM) {
+            cp_async_rec<8>(smem_u32(&s_c2[0][c]), v2 + pc);
+            s_lv[0][c] = (double)leaves[f + c];
+          }
+        }
       }
       cp_async_commit();
       cp_async_wait<0>();
+      if (D > 0) group_sync(g1, grp);
     }
-    __syncthreads();
-    // ---- the k levels, pairwise, in shared memory
-    int cur = 0, nl = C;
-    for (int lev = 0; lev < nlev && nl > 1; ++lev) {
-      const int nl2 = (nl + 1) >> 1;
-      const int* ls = s_ls[lev & 1];
-      int* ls2 = s_ls[(lev + 1) & 1];
-      if (tid <= nl2) ls2[tid] = tid < nl2 ? ls[2 * tid] : ls[nl];
-      if (MOM && tid < nl2 && 2 * tid + 1 < nl) {  // moments weights of output list tid
-        const double nA = s_lv[lev & 1][2 * tid], nB = s_lv[lev & 1][2 * tid + 1];
+    const T TINF = (T)INFINITY;
+    for (int L = 1; L <= D; ++L) {
+      const int gsz = (WTH / 32) >> (D - L);
+      const int li = warp / gsz;                 // this group's output list
+      const int ca0 = li << L;                   // its first child
+      if (L > 1) group_sync(gsz, li);            // its inputs (level L - 1) are complete
+      if (ca0 >= C) continue;                    // an empty list: nothing to merge
+      const int cmid = min(ca0 + (1 << (L - 1)), C), cend = min(ca0 + (1 << L), C);
+      const bool pass = cmid >= C;               // right subtree empty: passthrough
+      const int a0 = s_ls[0][ca0], b0 = s_ls[0][cmid], e0 = s_ls[0][cend];
+      const int na = b0 - a0, nb = e0 - b0;
+      // carries (and leaf counts) of the inputs: lists 2 li and 2 li + 1 of level L - 1
+      const VT cva = s_cv[L - 1][2 * li];
+      const VT cvb = pass ? VT(0) : s_cv[L - 1][2 * li + 1];
+      const double c2a = MOM ? s_c2[L - 1][2 * li] : 0.0;
+      const double c2b = (MOM && !pass) ? s_c2[L - 1][2 * li + 1] : 0.0;
+      double wB = 0.0, wAB = 0.0;
+      if (MOM && !pass) {
+        const double nA = s_lv[L - 1][2 * li], nB = s_lv[L - 1][2 * li + 1];
         const double n = nA + nB;
-        s_w[lev & 1][tid][0] = nB / n;
-        s_w[lev & 1][tid][1] = nA * nB / n;
+        wB = nB / n;
+        wAB = nA * nB / n;
       }
-      const T* it = bt(cur);
-      const VT* iv = bv(cur);
-      const double* i2 = b2(cur);
-      T* ot = bt(cur ^ 1);
-      VT* ov = bv(cur ^ 1);
-      double* o2 = b2(cur ^ 1);
-      const VT* cv = s_cv[lev & 1];
-      const double* c2 = s_c2[lev & 1];
-      const double* lv = s_lv[lev & 1];
-      __syncthreads();
-      const T TINF = (T)INFINITY;
-      for (int base = 0; base < E; base += WTH * WLPT) {
-        const int p0 = base + tid * WLPT;
+      const int r = tid - li * gsz * 32;         // rank in the group
+      if (r == 0) {  // this list's carry and leaf count for level L + 1
+        if (pass) {
+          s_cv[L][li] = cva;
+          if (MOM) {
+            s_c2[L][li] = c2a;
+            s_lv[L][li] = s_lv[L - 1][2 * li];
+          }
+        } else if (MOM) {
+          const double d = (double)cvb - (double)cva;
+          s_cv[L][li] = (VT)((double)cva + d * wB);
+          s_c2[L][li] = (c2a + c2b) + d * d * wAB;
+          s_lv[L][li] = s_lv[L - 1][2 * li] + s_lv[L - 1][2 * li + 1];
+        } else {
+          s_cv[L][li] = to_t<VT>(vop<K>((double)cva, (double)cvb));
+        }
+      }
+      const T* it = bt((L - 1) & 1);
+      const VT* iv = bv((L - 1) & 1);
+      const double* i2 = b2((L - 1) & 1);
+      T* ot = bt(L & 1);
+      VT* ov = bv(L & 1);
+      double* o2 = b2(L & 1);
+      for (int base = 0; base < na + nb; base += gsz * 32 * WLPT) {
+        const int m0 = base + r * WLPT;          // first output position (list-relative)
+        if (m0 >= na + nb) break;
+        int i, j;
+        if (pass) {
+          i = m0;
+          j = 0;
+        } else {
+          int lo = max(0, m0 - nb), hi = min(m0, na);
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (it[pad(a0 + mid)] <= it[pad(b0 + m0 - mid - 1)]) lo = mid + 1;
+            else hi = mid;
+          }
+          i = lo;
+          j = m0 - lo;
+        }
+        T tai = i < na ? it[pad(a0 + i)] : TINF;
+        T tbj = j < nb ? it[pad(b0 + j)] : TINF;
+        VT ca = i > 0 ? iv[pad(a0 + i - 1)] : cva;
+        VT cb = j > 0 ? iv[pad(b0 + j - 1)] : cvb;
+        double ca2 = MOM ? (i > 0 ? i2[pad(a0 + i - 1)] : c2a) : 0.0;
+        double cb2 = MOM ? (j > 0 ? i2[pad(b0 + j - 1)] : c2b) : 0.0;
         T o_t[WLPT];
         VT o_v[WLPT];
         double o_2[WLPT];
-        if (p0 < E) {
-          int li = 0;  // output list containing p0
-          {
-            int lo = 0, hi = nl2 - 1;
-            while (lo < hi) {
-              const int mid = (lo + hi + 1) >> 1;
-              if (ls2[mid] <= p0) lo = mid;
-              else hi = mid - 1;
-            }
-            li = lo;
-          }
-          // walk state: the next time of A and B (+inf past the end) and the values of A
-          // and B at the current point (their last consumed point, or their carry)
-          int a0 = 0, na = 0, b0 = 0, nb = 0, i = 0, j = 0;
-          bool pass = false;
-          T tai = TINF, tbj = TINF;
-          VT ca = VT(0), cb = VT(0);
-          double ca2 = 0.0, cb2 = 0.0, wB = 0.0, wAB = 0.0;
-          auto open = [&](int m) {
-            const ListPos L = open_list(ls, nl, li, m, it);
-            a0 = L.a0; na = L.na; b0 = L.b0; nb = L.nb; i = L.i; j = L.j;
-            pass = L.pass;
-            tai = i < na ? it[pad(a0 + i)] : TINF;
-            tbj = j < nb ? it[pad(b0 + j)] : TINF;
-            ca = i > 0 ? iv[pad(a0 + i - 1)] : cv[2 * li];
-            if (MOM) ca2 = i > 0 ? i2[pad(a0 + i - 1)] : c2[2 * li];
-            if (!pass) {
-              cb = j > 0 ? iv[pad(b0 + j - 1)] : cv[2 * li + 1];
-              if (MOM) {
-                cb2 = j > 0 ? i2[pad(b0 + j - 1)] : c2[2 * li + 1];
-                wB = s_w[lev & 1][li][0];
-                wAB = s_w[lev & 1][li][1];
-              }
-            }
-          };
-          open(p0 - ls2[li]);
 #pragma unroll
-          for (int qq = 0; qq < WLPT; ++qq) {
-            const int p = p0 + qq;
-            if (p < E) {
-              if (li + 1 < nl2 && p >= ls2[li + 1]) {
-                ++li;  // the next non-empty list (a sub-window can leave lists empty)
-                while (li + 1 < nl2 && p >= ls2[li + 1]) ++li;
-                open(0);
-              }
-              const bool takeA = tai <= tbj;  // A first on ties
-              if (takeA) {
-                o_t[qq] = tai;
-                ca = iv[pad(a0 + i)];
-                if (MOM) ca2 = i2[pad(a0 + i)];
-                ++i;
-                tai = i < na ? it[pad(a0 + i)] : TINF;
-              } else {
-                o_t[qq] = tbj;
-                cb = iv[pad(b0 + j)];
-                if (MOM) cb2 = i2[pad(b0 + j)];
-                ++j;
-                tbj = j < nb ? it[pad(b0 + j)] : TINF;
-              }
-              if (pass) {
-                o_v[qq] = ca;
-                if (MOM) o_2[qq] = ca2;
-              } else if (MOM) {
-                const double d = (double)cb - (double)ca;
-                o_v[qq] = (VT)((double)ca + d * wB);
-                o_2[qq] = (ca2 + cb2) + d * d * wAB;
-              } else {
-                o_v[qq] = to_t<VT>(vop<K>((double)ca, (double)cb));
-              }
+        for (int q = 0; q < WLPT; ++q) {
+          if (m0 + q < na + nb) {
+            const bool takeA = tai <= tbj;  // A first on ties
+            if (takeA) {
+              o_t[q] = tai;
+              ca = iv[pad(a0 + i)];
+              if (MOM) ca2 = i2[pad(a0 + i)];
+              ++i;
+              tai = i < na ? it[pad(a0 + i)] : TINF;
+            } else {
+              o_t[q] = tbj;
+              cb = iv[pad(b0 + j)];
+              if (MOM) cb2 = i2[pad(b0 + j)];
+              ++j;
+              tbj = j < nb ? it[pad(b0 + j)] : TINF;
             }
-          }
-#pragma unroll
-          for (int qq = 0; qq < WLPT; ++qq) {
-            if (p0 + qq < E) {
-              const int y = pad(p0 + qq);
-              ot[y] = o_t[qq];
-              ov[y] = o_v[qq];
-              if (MOM) o2[y] = o_2[qq];
+            if (pass) {
+              o_v[q] = ca;
+              if (MOM) o_2[q] = ca2;
+            } else if (MOM) {
+              const double d = (double)cb - (double)ca;
+              o_v[q] = (VT)((double)ca + d * wB);
+              o_2[q] = (ca2 + cb2) + d * d * wAB;
+            } else {
+              o_v[q] = to_t<VT>(vop<K>((double)ca, (double)cb));
             }
           }
         }
-      }
-      // carries and leaf counts of the merged lists
-      if (tid < nl2) {
-        VT* ncv = s_cv[(lev + 1) & 1];
-        double* nc2 = s_c2[(lev + 1) & 1];
-        double* nlv = s_lv[(lev + 1) & 1];
-        if (2 * tid + 1 >= nl) {
-          ncv[tid] = cv[2 * tid];
-          if (MOM) {
-            nc2[tid] = c2[2 * tid];
-            nlv[tid] = lv[2 * tid];
+#pragma unroll
+        for (int q = 0; q < WLPT; ++q) {
+          if (m0 + q < na + nb) {
+            const int y = pad(a0 + m0 + q);
+            ot[y] = o_t[q];
+            ov[y] = o_v[q];
+            if (MOM) o2[y] = o_2[q];
           }
-        } else if (MOM) {
-          const double nA = lv[2 * tid], nB = lv[2 * tid + 1];
-          const double n = nA + nB;
-          const double va = cv[2 * tid], vb = cv[2 * tid + 1];
-          const double d = vb - va;
-          ncv[tid] = (VT)(va + d * (nB / n));
-          nc2[tid] = (c2[2 * tid] + c2[2 * tid + 1]) + d * d * (nA * nB / n);
-          nlv[tid] = n;
-        } else {
-          ncv[tid] = to_t<VT>(vop<K>((double)cv[2 * tid], (double)cv[2 * tid + 1]));
         }
       }
-      __syncthreads();
-      cur ^= 1;
-      nl = nl2;
     }
+    __syncthreads();
+    const int cur = D & 1;
     // ---- the merged window, written once (coalesced)
     {
       const T* st = bt(cur);
