@@ -279,8 +279,8 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
     fuse = max(1, min(4, int(fuse_env))) if fuse_env else (1 if moments else 4)
     pkey = (None if leaves0 is not None or np.asarray(seg_nodes).size > 64 else
             (tuple(int(x) for x in np.asarray(seg_nodes)), bool(moments), str(dev)))
-    merge0 = False  # level 0 too runs non-compacting (fused with the levels above it)
-    if mode == "auto" and fuse > 1 and len(plan) > 1 and level.nnodes >= 2:
+    merge0 = False  # level 0 too runs non-compacting (fused with the levels above it, if any)
+    if mode == "auto" and len(plan) > 1 and level.nnodes >= 2:
         # a sample of neighbouring leaf pairs: nearly distinct breakpoints mean compaction
         # would drop (almost) nothing, so every level can be a fused merge
         counts = _scratch("dup", 2, torch.int64, dev)
@@ -290,7 +290,7 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
                                               st), "pcf_tree_dup_sample")
         dup, seen = (int(x) for x in counts.cpu())
         merge0 = merge = seen > 0 and dup <= 0.02 * seen
-    elif mode == "merge" and fuse > 1:
+    elif mode == "merge":
         merge0 = True
     li = 0
     nbuf = 0
@@ -332,7 +332,7 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
                 nout, bound, _native.ptr(t_out), _native.ptr(v_out),
                 _native.ptr(m2_out) if moments else None, _native.ptr(off_out), _native.ptr(ws),
                 ws.numel())
-        if merge and li > 0:
+        if merge and (li > 0 or merge0):
             # non-compacting merge (zero-width pieces are dropped by _finalize)
             _native.check(lib.pcf_tree_merge_level(kind, *args, st), "pcf_tree_merge_level")
         else:
