@@ -16,7 +16,8 @@
  * plus the whole-matrix path the GPU needs (MatrixJob.run's block loop,
  * pkg/src/pcflib/matrix.py:156-234, moved on-device): pcf_plan_pairwise + pcf_fill_matrix,
  * and the reduction path that has no boundary in the reference (reduce.py:31-63,189-238):
- * pcf_tree_level (+ pcf_scale_flag / pcf_std_flag / pcf_compact to finalise).
+ * pcf_tree_level / pcf_tree_merge_level(s) per level, pcf_finalize to finalise (the older
+ * flag + compact pair pcf_scale_flag / pcf_std_flag + pcf_compact remains available).
  *
  * Conventions
  *  - All functions return PCF_OK (0) or an error code; pcf_last_error() gives the text.
@@ -269,8 +270,9 @@ int pcf_probe_fp64(double* out_dev, int iters, int blocks_per_sm, void* stream);
  * sweep directly); these entry points are the device replacement.  A tree level maps
  * nodes (SoA times/values, int64 offsets) to output nodes: output k merges input nodes
  * src[k], src[k]+1 (cnt[k]=2) or passes src[k] through (cnt[k]=1).
- * pcf_compact: exclusive scan of keep flags (ntot candidates) + scatter of the kept points,
- * used by the finalisation (pcf_scale_flag / pcf_std_flag). */
+ * pcf_compact: exclusive scan of keep flags (ntot candidates, tiled; no library scan) +
+ * scatter of the kept points + output node offsets (after pcf_scale_flag / pcf_std_flag;
+ * pcf_finalize does flag + compact in one call without the flag arrays). */
 int pcf_scan_workspace(int64_t ntot, int64_t* bytes);
 /* value_bytes: element size of sv/sv2 (4 or 8); sv2 may be NULL. */
 int pcf_compact(int is_f32, const void* st_dev, const void* sv_dev, const void* sv2_dev,

@@ -150,3 +150,40 @@ def test_distributed_reductions_single_rank_match(tmp_path):
     m1, s1 = mean_packed(lvl), std_packed(lvl)
     assert torch.equal(m.t[: m.ntot], m1.t[: m1.ntot]) and torch.equal(m.v[: m.ntot], m1.v[: m1.ntot])
     assert torch.equal(s.v[: s.ntot], s1.v[: s1.ntot])
+
+
+def test_flag_compact_pair_matches_finalize():
+    """The two-call finalisation (pcf_scale_flag + pcf_compact, tiled scan) and the
+    one-call pcf_finalize give the same minimised mean."""
+    import torch
+
+    from paper_2404_07183_b200 import _native
+    from paper_2404_07183_b200.reduce import DeviceLevel, _run_tree
+
+    fs = pb.noisy_sin((300,), 40, rng=pb.RngSpec(6)).to_list()
+    lvl, _ = _run_tree(DeviceLevel.from_pcfs(fs), [300], op=0)
+    lib = _native.load()
+    n, dev = lvl.ntot, lvl.t.device
+    sc = torch.tensor([1.0 / 300], dtype=torch.float64, device=dev)
+    sv = torch.empty(n, dtype=torch.float64, device=dev)
+    flag = torch.empty(n, dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _native.check(lib.pcf_scale_flag(0, _native.ptr(lvl.v), _native.ptr(lvl.t), _native.ptr(lvl.off),
+                                     1, _native.ptr(sc), n, _native.ptr(sv), _native.ptr(flag),
+                                     _native.ptr(status), None), "flag")
+    nb = _native.c_i64(0)
+    lib.pcf_scan_workspace(n, _native.ctypes.byref(nb))
+    tmp = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+    pos = torch.empty(n, dtype=torch.int64, device=dev)
+    t_out = torch.empty(n, dtype=torch.float64, device=dev)
+    v_out = torch.empty(n, dtype=torch.float64, device=dev)
+    off_out = torch.empty(2, dtype=torch.int64, device=dev)
+    src = torch.zeros(1, dtype=torch.int64, device=dev)
+    _native.check(lib.pcf_compact(0, _native.ptr(lvl.t), _native.ptr(sv), None, 8,
+                                  _native.ptr(flag), n, _native.ptr(lvl.off), _native.ptr(src), 1,
+                                  _native.ptr(pos), _native.ptr(tmp), tmp.numel(),
+                                  _native.ptr(t_out), _native.ptr(v_out), None,
+                                  _native.ptr(off_out), None), "compact")
+    k = int(off_out[1].item())
+    got = np.column_stack((t_out[:k].cpu().numpy(), v_out[:k].cpu().numpy()))
+    assert np.array_equal(got, pb.mean(fs).to_matrix())
