@@ -18,9 +18,15 @@ t, v, off = dg.synthetic_benchmark_packed(M, rng=dg.RngSpec(2404))
 ht = torch.from_numpy(t).pin_memory()
 hv = torch.from_numpy(v).pin_memory()
 ho = torch.from_numpy(off).pin_memory()
-out = torch.empty((M, M), dtype=torch.float64, pin_memory=True)
+# PCF_E2E_PAGEABLE=1: a plain numpy result (rows through pcf_matrix_host's staging pool)
+if os.environ.get("PCF_E2E_PAGEABLE"):
+    out = np.empty((M, M), dtype=np.float64)
+else:
+    out = torch.empty((M, M), dtype=torch.float64, pin_memory=True)
 for nc in chunks:
     for rep in range(2):
         t0 = time.perf_counter()
         matrix_host(ht.numpy(), hv.numpy(), ho.numpy(), 0, 1.0, True, False, n_chunks=nc, out=out)
+        if rep == 0 and os.environ.get("PCF_E2E_PAGEABLE"):
+            print("  (first call: includes first-touch page faults of the result)", flush=True)
         print(f"chunks={nc} rep={rep} wall {time.perf_counter() - t0:.3f} s", flush=True)
