@@ -505,20 +505,25 @@ __global__ void __launch_bounds__(WTH, 3)
 #pragma unroll
         for (int q = 0; q < WLPT; ++q) {
           if (m0 + q < na + nb) {
+            // branch-free step: the consumed list's point (value) and its next time are
+            // the only loads; selects route them to A's or B's state
             const bool takeA = tai <= tbj;  // A first on ties
-            if (takeA) {
-              o_t[q] = tai;
-              ca = iv[pad(a0 + i)];
-              if (MOM) ca2 = i2[pad(a0 + i)];
-              ++i;
-              tai = i < na ? it[pad(a0 + i)] : TINF;
-            } else {
-              o_t[q] = tbj;
-              cb = iv[pad(b0 + j)];
-              if (MOM) cb2 = i2[pad(b0 + j)];
-              ++j;
-              tbj = j < nb ? it[pad(b0 + j)] : TINF;
+            const int x = takeA ? a0 + i : b0 + j;
+            const int xe = takeA ? a0 + na : b0 + nb;
+            o_t[q] = takeA ? tai : tbj;
+            const VT val = iv[pad(x)];
+            const T nt = x + 1 < xe ? it[pad(x + 1)] : TINF;
+            ca = takeA ? val : ca;
+            cb = takeA ? cb : val;
+            tai = takeA ? nt : tai;
+            tbj = takeA ? tbj : nt;
+            if (MOM) {
+              const double v2x = i2[pad(x)];
+              ca2 = takeA ? v2x : ca2;
+              cb2 = takeA ? cb2 : v2x;
             }
+            i += takeA ? 1 : 0;
+            j += takeA ? 0 : 1;
             if (pass) {
               o_v[q] = ca;
               if (MOM) o_2[q] = ca2;
