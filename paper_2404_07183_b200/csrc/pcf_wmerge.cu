@@ -499,9 +499,6 @@ __global__ void __launch_bounds__(WTH, 3)
         VT cb = j > 0 ? iv[pad(b0 + j - 1)] : cvb;
         double ca2 = MOM ? (i > 0 ? i2[pad(a0 + i - 1)] : c2a) : 0.0;
         double cb2 = MOM ? (j > 0 ? i2[pad(b0 + j - 1)] : c2b) : 0.0;
-        T o_t[WLPT];
-        VT o_v[WLPT];
-        double o_2[WLPT];
 #pragma unroll
         for (int q = 0; q < WLPT; ++q) {
           if (m0 + q < na + nb) {
@@ -510,7 +507,8 @@ __global__ void __launch_bounds__(WTH, 3)
             const bool takeA = tai <= tbj;  // A first on ties
             const int x = takeA ? a0 + i : b0 + j;
             const int xe = takeA ? a0 + na : b0 + nb;
-            o_t[q] = takeA ? tai : tbj;
+            const int y = pad(a0 + m0 + q);  // the output buffer is the other ping-pong half
+            ot[y] = takeA ? tai : tbj;
             const VT val = iv[pad(x)];
             const T nt = x + 1 < xe ? it[pad(x + 1)] : TINF;
             ca = takeA ? val : ca;
@@ -525,24 +523,15 @@ __global__ void __launch_bounds__(WTH, 3)
             i += takeA ? 1 : 0;
             j += takeA ? 0 : 1;
             if (pass) {
-              o_v[q] = ca;
-              if (MOM) o_2[q] = ca2;
+              ov[y] = ca;
+              if (MOM) o2[y] = ca2;
             } else if (MOM) {
               const double d = (double)cb - (double)ca;
-              o_v[q] = (VT)((double)ca + d * wB);
-              o_2[q] = (ca2 + cb2) + d * d * wAB;
+              ov[y] = (VT)((double)ca + d * wB);
+              o2[y] = (ca2 + cb2) + d * d * wAB;
             } else {
-              o_v[q] = to_t<VT>(vop<K>((double)ca, (double)cb));
+              ov[y] = to_t<VT>(vop<K>((double)ca, (double)cb));
             }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < WLPT; ++q) {
-          if (m0 + q < na + nb) {
-            const int y = pad(a0 + m0 + q);
-            ot[y] = o_t[q];
-            ov[y] = o_v[q];
-            if (MOM) o2[y] = o_2[q];
           }
         }
       }

@@ -272,11 +272,10 @@ def _run_tree(level: DeviceLevel, seg_nodes, op=None, moments=False, leaves0=Non
     nout = level.nnodes
     mode = os.environ.get("PCF_TREE_MODE", "auto")  # auto | compact | merge
     merge = mode == "merge"
-    # levels per fused pass (pcf_tree_merge_levels, K5w): the sum/max/min/mul trees gain from
-    # 4 (c5 mean 18.3 -> 17.1 ms); the moments tree (24-byte points, smaller tiles) runs
-    # faster level by level (26.6 vs 29.0 ms), so it defaults to 1
+    # levels per fused pass (pcf_tree_merge_levels, K5w): 4 (c5 mean 26 -> 14.1 ms, c5 std
+    # 26.5 -> 22.4 ms against one launch per level)
     fuse_env = os.environ.get("PCF_TREE_FUSE")
-    fuse = max(1, min(4, int(fuse_env))) if fuse_env else (1 if moments else 4)
+    fuse = max(1, min(4, int(fuse_env))) if fuse_env else 4
     pkey = (None if leaves0 is not None or np.asarray(seg_nodes).size > 64 else
             (tuple(int(x) for x in np.asarray(seg_nodes)), bool(moments), str(dev)))
     merge0 = False  # level 0 too runs non-compacting (fused with the levels above it, if any)
