@@ -14,7 +14,10 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpcfb200.so")
+# PCF_LIB_VARIANT=name loads _lib/libpcfb200.<name>.so (tools/build_variant.py: the same
+# library with one translation unit rebuilt under extra -D flags, for tuning sweeps)
+LIB_PATH = os.path.join(_HERE, "_lib", "libpcfb200.so" if not os.environ.get("PCF_LIB_VARIANT")
+                        else f"libpcfb200.{os.environ['PCF_LIB_VARIANT']}.so")
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
