@@ -261,6 +261,32 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     }
     const int pair_id = (cc * RG + rho) * GW + u;  // 0 .. GW*RG*C-1
     const int npairs = GW * RG * C;
+    // Per-chunk global metadata (the lane's column size and offset in the chunk, the
+    // output indices) is loaded one chunk ahead, so no warp starts a chunk's walk -- or a
+    // finisher its stores -- behind an L2 round trip (long-scoreboard stalls at every chunk
+    // start otherwise; all warps reach it together after the chunk barrier).
+    const int fu = tid & (GW - 1), frho = (tid >> LOGGW) & (RG - 1);
+    const int fcc = tid >> (LOGGW + logRG);
+    const int fps = W.row0 + GW * frho + fu;   // finisher's row (G > 1, tid < npairs)
+    const int64_t fpi = (G > 1 && tid < npairs && fps < M) ? (int64_t)perm[fps] : 0;
+    int m_ng = 0, m_go = 0;
+    int64_t m_pq = 0;
+    auto load_meta = [&](int c) {
+      const int cb = W.col0 + (c << logC), ce = min(cb + C, W.col1);
+      const int qs = cb + cc;
+      m_ng = 0; m_go = 0; m_pq = 0;
+      if (row_ok && qs < ce && qs > ps && g < G) {
+        const int64_t s0 = soff[qs];
+        m_ng = (int)(soff[qs + 1] - s0);
+        m_go = (int)(s0 - cstart(cb));
+        if (G == 1) m_pq = perm[qs];
+      }
+      if (G > 1 && tid < npairs) {
+        const int pqs = cb + fcc;
+        if (fps < M && pqs < ce && pqs > fps) m_pq = perm[pqs];
+      }
+    };
+    if (nchunk > 0) load_meta(0);
     mbar_wait(&bars[0], ph_row);
     ph_row ^= 1u;
 
@@ -272,6 +298,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const int qs = cb + cc;
       // g >= G: an idle quarter (exact-mode items with fewer than 64 row x column lanes)
       const bool ok = row_ok && qs < ce && qs > ps && g < G;
+      const int ng = m_ng, go = m_go;
+      const int64_t pq = m_pq;
+      if (c + 1 < nchunk) load_meta(c + 1);  // in flight during this chunk's walk
       mbar_wait(&bars[1 + kb], ph_col[kb]);
       ph_col[kb] ^= 1u;
       if (single && tid == 0 && c + 1 < nchunk) {
@@ -283,13 +312,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const RT* Gv = reinterpret_cast<const RT*>(colbase + kb * col_al);
       double acc = 0.0, hl = 0.0;
       if (ok) {
-        const int ng = (int)(soff[qs + 1] - soff[qs]);
-        Gv += soff[qs] - cstart(cb);
+        Gv += go;
         acc = lane_walk<HK, BOUNDED, GW, 1, RT>(F, nf, Gv, ng, g, log2G, p, a, b);
         if (!BOUNDED) hl = hval<HK>(F[(nf - 1) * GW].v, Gv[ng - 1].v, p);
       }
       if (G == 1) {
-        if (ok) finish_entry<HK, BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
+        if (ok) finish_entry<HK, BOUNDED, OutT>(acc, hl, p, apply_root, oi, pq, out, ld, M, err);
         __syncthreads();  // column buffer `kb` is free again
         if (tid == 0 && c + ncb < nchunk) issue(c + ncb);
       } else {
@@ -298,15 +326,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         __syncthreads();  // partials visible, column buffer `kb` free again
         if (tid == 0 && c + ncb < nchunk) issue(c + ncb);  // before finishing: keep TMA busy
         if (tid < npairs) {
-          const int pu = tid & (GW - 1), prho = (tid >> LOGGW) & (RG - 1);
-          const int pcc = tid >> (LOGGW + logRG);
-          const int pps = W.row0 + GW * prho + pu, pqs = cb + pcc;
-          if (pps < M && pqs < ce && pqs > pps) {
+          const int pqs = cb + fcc;
+          if (fps < M && pqs < ce && pqs > fps) {
             const double* r = red + buf * kTileThreads + tid;
             double s = r[0];
             for (int k = 1; k < G; ++k) s = __dadd_rn(s, r[k * npairs]);
             finish_entry<HK, BOUNDED, OutT>(s, redh[buf * kTileThreads + tid], p, apply_root,
-                                        perm[pps], perm[pqs], out, ld, M, err);
+                                        fpi, pq, out, ld, M, err);
           }
         }
       }
