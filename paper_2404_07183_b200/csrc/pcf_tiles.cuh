@@ -35,6 +35,13 @@ namespace pcfb {
 // Bounded b: cell right edges are clamped to b (cells past b become zero-width) and the
 // last lane adds the final cell h(v_f_last, v_g_last) * (b - t).  Unbounded b: the tail
 // cell is left to the caller, which applies the divergence rule of pyx:47-51.
+#ifndef PCF_K1_ICMP
+#define PCF_K1_ICMP 0
+#endif
+#ifndef PCF_K1_UNROLL
+#define PCF_K1_UNROLL 8
+#endif
+constexpr int kK1Unroll = PCF_K1_UNROLL;
 template <int HK, bool BOUNDED, int SF, int SG, typename RT = Rec>
 __device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
                                             const RT* __restrict__ Gv, int ng, int lane,
@@ -91,7 +98,7 @@ __device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
   double acc = 0.0;
   double hc = hval<HK>((double)vx, (double)vy, p);
   const int steps = d1 - d0;
-#pragma unroll 4
+#pragma unroll kK1Unroll
   for (int s = 0; s < steps; ++s) {
     double tn = (double)tx;
     if (BOUNDED) tn = fmin(tn, b);
@@ -107,7 +114,14 @@ __device__ __forceinline__ double lane_walk(const RT* __restrict__ F, int nf,
     xp += xs;
     const ST nt = xp->t, nv = xp->v;
     hc = hval<HK>((double)nv, (double)vy, p);
-    const bool sw = nt > ty;
+    bool sw;
+    if constexpr (sizeof(ST) == 8 && PCF_K1_ICMP) {
+      // record times are piece END times: > 0 or +inf, never NaN or -0, so the IEEE
+      // order is the order of the bit patterns as signed integers (ALU, not the FP64 pipe)
+      sw = __double_as_longlong((double)nt) > __double_as_longlong((double)ty);
+    } else {
+      sw = nt > ty;
+    }
     const RT* __restrict__ np = sw ? yp : xp;
     yp = sw ? xp : yp;
     xp = np;
