@@ -153,7 +153,8 @@ class Stager {
       free_.push_back(k);
     }
     const unsigned hw = std::thread::hardware_concurrency();
-    const int nw = (int)std::max(2u, std::min(16u, hw ? hw / 2 : 4u));
+    int nw = (int)std::max(2u, std::min(16u, hw ? hw : 4u));
+    if (const char* ev = getenv("PCF_STAGE_WORKERS")) nw = std::max(1, atoi(ev));
     for (int w = 0; w < nw; ++w) workers_.emplace_back([this] { work(); });
   }
   ~Stager() { finish(); }
@@ -536,8 +537,13 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   std::unique_ptr<Stager> stager;
   if (!pinned_out) {
     const size_t row = (size_t)M * es;
-    const size_t slot_rows = std::max<size_t>(1, std::min<size_t>((size_t)M, (128u << 20) / row));
-    const int nslot = 8;
+    // 16 x 64 MB slots, one host copy thread per core (<= 16): c3 drain after the fill
+    // 133 -> 120 ms against 8 x 128 MB with hw / 2 threads (tools/time_stage.py)
+    size_t slot_mb = 64;
+    int nslot = 16;
+    if (const char* ev = getenv("PCF_STAGE_MB")) slot_mb = std::max(1, atoi(ev));
+    if (const char* ev = getenv("PCF_STAGE_SLOTS")) nslot = std::max(2, atoi(ev));
+    const size_t slot_rows = std::max<size_t>(1, std::min<size_t>((size_t)M, (slot_mb << 20) / row));
     char* pool = nullptr;
     if ((e = g_pin.get((size_t)nslot * slot_rows * row, &pool)))
       return cudaStreamSynchronize(s0), fail(e, "pcf_matrix_host staging pool");
