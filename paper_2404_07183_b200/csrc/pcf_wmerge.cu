@@ -43,6 +43,9 @@ constexpr int WTH = 256;   // threads per tile CTA (192, or 128 with 1024-point 
 #ifndef PCF_WLPT
 #define PCF_WLPT 8
 #endif
+#ifndef PCF_WM_PRED
+#define PCF_WM_PRED 1
+#endif
 constexpr int KMAXC = 16;  // children per output node (k <= 4 levels per pass)
 constexpr int kTreeTgt = 512;  // points per K5t tile (one thread each)
 enum { K_ADD = 0, K_MAX = 1, K_MIN = 2, K_MUL = 3, K_MOM = 4 };
@@ -511,35 +514,47 @@ __global__ void __launch_bounds__(WTH, 3)
         // one merge step at output position m = m0 + q, branch-free: the consumed list's
         // point (value) and its next time are the only loads; selects route them to A's
         // or B's state.  The output buffer is the other ping-pong half.
-        auto step = [&](int m) {
+        auto step = [&](int m, bool live) {
           const bool takeA = tai <= tbj;  // A first on ties
           const int x = takeA ? a0 + i : b0 + (m - i);
           const int xe = takeA ? b0 : e0;
           const int y = pad(a0 + m);
-          ot[y] = takeA ? tai : tbj;
+          if (live) ot[y] = takeA ? tai : tbj;
           const VT val = iv[pad(x)];
           const T nt = x + 1 < xe ? it[pad(x + 1)] : TINF;
           ca = takeA ? val : ca;
           cb = takeA ? cb : val;
           tai = takeA ? nt : tai;
           tbj = takeA ? tbj : nt;
-          i += takeA ? 1 : 0;
+          // past the list's end both times are +inf and takeA holds: i stops at na, so
+          // the dead steps re-read B's first point (this list's own input, never another
+          // group's) and store nothing
+          i += (takeA && i < na) ? 1 : 0;
           if (MOM) {
             const double v2x = i2[pad(x)];
             ca2 = takeA ? v2x : ca2;
             cb2 = takeA ? cb2 : v2x;
             const double d = (double)cb - (double)ca;
-            ov[y] = (VT)((double)ca + d * wB);
-            o2[y] = (ca2 + cb2) + d * d * wAB;
+            if (live) {
+              ov[y] = (VT)((double)ca + d * wB);
+              o2[y] = (ca2 + cb2) + d * d * wAB;
+            }
           } else {
-            ov[y] = to_t<VT>(vop<K>((double)ca, (double)cb));
+            if (live) ov[y] = to_t<VT>(vop<K>((double)ca, (double)cb));
           }
         };
+#if PCF_WM_PRED
+        // one unrolled body, the list's tail handled by predicated stores (no per-step
+        // branch and reconvergence)
+#pragma unroll
+        for (int q = 0; q < WLPT; ++q) step(m0 + q, m0 + q < na + nb);
+#else
         // (one guarded unrolled loop: splitting off an unguarded full-WLPT path measured
         // slower, 14.6 vs 13.9 ms on c5 mean)
 #pragma unroll
         for (int q = 0; q < WLPT; ++q)
-          if (m0 + q < na + nb) step(m0 + q);
+          if (m0 + q < na + nb) step(m0 + q, true);
+#endif
       }
     }
     __syncthreads();
