@@ -566,7 +566,11 @@ constexpr int kRingThreads = 640;
 #ifndef PCF_RING_L1
 #define PCF_RING_L1 0
 #endif
-constexpr bool kRingL1 = PCF_RING_L1;  // refills through L1 (.ca): neighbours share a line
+constexpr bool kRingL1 = PCF_RING_L1;
+#ifndef PCF_RING_UNROLL
+#define PCF_RING_UNROLL 2
+#endif
+constexpr int kRingUnroll = PCF_RING_UNROLL;  // step pairs per unrolled iteration  // refills through L1 (.ca): neighbours share a line
 
 // The walk of one lane over merge-path segment `lane` of 2^log2G (G = 1: the whole pair,
 // left to right -- the reference's sum) with the row in shared memory (stride SF records:
@@ -681,7 +685,7 @@ __device__ __forceinline__ double lane_walk_ring(const RT* __restrict__ F, int n
     // one commit group per two steps: a record read at step s was requested at step
     // <= s - (D - 1), i.e. in a group at least 3 groups old, so waiting until <= 2 groups
     // are pending before each pair of steps covers both
-#pragma unroll 2
+#pragma unroll kRingUnroll
     for (; s + 1 < steps; s += 2) {
       cp_async_wait<(D - 3) / 2>();
       step();
