@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (ok) {
         Gv += go;
         acc = lane_walk<HK, BOUNDED, GW, 1, RT>(F, nf, Gv, ng, g, log2G, p, a, b);
-        if (!BOUNDED) hl = hval<HK>(F[(nf - 1) * GW].v, Gv[ng - 1].v, p);
+        if (!BOUNDED && g == 0) hl = hval<HK>(F[(nf - 1) * GW].v, Gv[ng - 1].v, p);
       }
       if (G == 1) {
         if (ok) finish_entry<HK, BOUNDED, OutT>(acc, hl, p, apply_root, oi, pq, out, ld, M, err);
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                        (goff[k] - goff[kbase]) + u;
         const int ng = (int)(soff[qs + 1] - soff[qs]);
         acc = lane_walk<HK, BOUNDED, 1, GW, RT>(F, nf, Gv, ng, g, log2G, p, a, b);
-        if (!BOUNDED) hl = hval<HK>(F[nf - 1].v, Gv[(ng - 1) * GW].v, p);
+        if (!BOUNDED && g == 0) hl = hval<HK>(F[nf - 1].v, Gv[(ng - 1) * GW].v, p);
       }
       if (G == 1) {
         if (ok) finish_entry<HK, BOUNDED, OutT>(acc, hl, p, apply_root, oi, perm[qs], out, ld, M, err);
