@@ -46,6 +46,9 @@ constexpr int WTH = 256;   // threads per tile CTA (192, or 128 with 1024-point 
 #ifndef PCF_WM_PRED
 #define PCF_WM_PRED 1
 #endif
+#ifndef PCF_WM_MOM16
+#define PCF_WM_MOM16 1
+#endif
 constexpr int KMAXC = 16;  // children per output node (k <= 4 levels per pass)
 constexpr int kTreeTgt = 512;  // points per K5t tile (one thread each)
 enum { K_ADD = 0, K_MAX = 1, K_MIN = 2, K_MUL = 3, K_MOM = 4 };
@@ -310,6 +313,13 @@ __global__ void __launch_bounds__(WTH, 3)
   auto b2 = [&](int k) {
     return reinterpret_cast<double*>(dyn + k * CP * C_::EB + CP * (int)(sizeof(T) + sizeof(VT)));
   };
+  // moments tree, paired layout: (mean, M2) of a point side by side as one 16-byte slot
+  // in the value region (same bytes as v[CP] | v2[CP]): one 16-byte load and store per
+  // merge step instead of two 8-byte ones each
+  constexpr bool P2 = MOM && PCF_WM_MOM16;
+  auto bp = [&](int k) {
+    return reinterpret_cast<double2*>(dyn + k * CP * C_::EB + CP * (int)sizeof(T));
+  };
   __shared__ int64_t s_cb[KMAXC];                 // first input position of each child
   __shared__ int s_lo[KMAXC], s_hi[KMAXC], s_end[KMAXC];
   __shared__ int s_ls[2][KMAXC + 1];              // s_ls[0]: children spans in the buffers
@@ -423,8 +433,14 @@ __global__ void __launch_bounds__(WTH, 3)
         for (int x = x0 + r; x < x1; x += g1 * 32) {
           const int y = pad(x);
           cp_async_rec<sizeof(T)>(smem_u32(st + y), gt + x);
-          cp_async_rec<sizeof(VT)>(smem_u32(sv + y), gv + x);
-          if (MOM) cp_async_rec<8>(smem_u32(s2 + y), g2 + x);
+          if (P2) {
+            const uint32_t pa = smem_u32(bp(0) + y);
+            cp_async_rec<8>(pa, gv + x);
+            cp_async_rec<8>(pa + 8u, g2 + x);
+          } else {
+            cp_async_rec<sizeof(VT)>(smem_u32(sv + y), gv + x);
+            if (MOM) cp_async_rec<8>(smem_u32(s2 + y), g2 + x);
+          }
         }
         if (r == 0) {  // the child's point before the window (its first point at 0)
           const int64_t pc = s_cb[c] + (s_lo[c] > 0 ? s_lo[c] - 1 : 0);
@@ -490,8 +506,12 @@ __global__ void __launch_bounds__(WTH, 3)
         for (int x = r; x < na; x += gsz * 32) {
           const int y = pad(a0 + x);
           ot[y] = it[y];
-          ov[y] = iv[y];
-          if (MOM) o2[y] = i2[y];
+          if (P2) {
+            bp(L & 1)[y] = bp((L - 1) & 1)[y];
+          } else {
+            ov[y] = iv[y];
+            if (MOM) o2[y] = i2[y];
+          }
         }
         continue;
       }
@@ -507,10 +527,21 @@ __global__ void __launch_bounds__(WTH, 3)
         int i = lo;  // A points consumed; B points consumed = (output position) - i
         T tai = i < na ? it[pad(a0 + i)] : TINF;
         T tbj = m0 - i < nb ? it[pad(b0 + m0 - i)] : TINF;
-        VT ca = i > 0 ? iv[pad(a0 + i - 1)] : cva;
-        VT cb = m0 - i > 0 ? iv[pad(b0 + m0 - i - 1)] : cvb;
-        double ca2 = MOM ? (i > 0 ? i2[pad(a0 + i - 1)] : c2a) : 0.0;
-        double cb2 = MOM ? (m0 - i > 0 ? i2[pad(b0 + m0 - i - 1)] : c2b) : 0.0;
+        VT ca, cb;
+        double ca2, cb2;
+        const double2* ip = bp((L - 1) & 1);
+        double2* op = bp(L & 1);
+        if (P2) {
+          const double2 pa = i > 0 ? ip[pad(a0 + i - 1)] : make_double2((double)cva, c2a);
+          const double2 pb = m0 - i > 0 ? ip[pad(b0 + m0 - i - 1)] : make_double2((double)cvb, c2b);
+          ca = (VT)pa.x; ca2 = pa.y;
+          cb = (VT)pb.x; cb2 = pb.y;
+        } else {
+          ca = i > 0 ? iv[pad(a0 + i - 1)] : cva;
+          cb = m0 - i > 0 ? iv[pad(b0 + m0 - i - 1)] : cvb;
+          ca2 = MOM ? (i > 0 ? i2[pad(a0 + i - 1)] : c2a) : 0.0;
+          cb2 = MOM ? (m0 - i > 0 ? i2[pad(b0 + m0 - i - 1)] : c2b) : 0.0;
+        }
         // one merge step at output position m = m0 + q, branch-free: the consumed list's
         // point (value) and its next time are the only loads; selects route them to A's
         // or B's state.  The output buffer is the other ping-pong half.
@@ -520,7 +551,9 @@ __global__ void __launch_bounds__(WTH, 3)
           const int xe = takeA ? b0 : e0;
           const int y = pad(a0 + m);
           if (live) ot[y] = takeA ? tai : tbj;
-          const VT val = iv[pad(x)];
+          double2 pv;
+          if (P2) pv = ip[pad(x)];
+          const VT val = P2 ? (VT)pv.x : iv[pad(x)];
           const T nt = x + 1 < xe ? it[pad(x + 1)] : TINF;
           ca = takeA ? val : ca;
           cb = takeA ? cb : val;
@@ -531,13 +564,17 @@ __global__ void __launch_bounds__(WTH, 3)
           // group's) and store nothing
           i += (takeA && i < na) ? 1 : 0;
           if (MOM) {
-            const double v2x = i2[pad(x)];
+            const double v2x = P2 ? pv.y : i2[pad(x)];
             ca2 = takeA ? v2x : ca2;
             cb2 = takeA ? cb2 : v2x;
             const double d = (double)cb - (double)ca;
             if (live) {
-              ov[y] = (VT)((double)ca + d * wB);
-              o2[y] = (ca2 + cb2) + d * d * wAB;
+              if (P2) {
+                op[y] = make_double2((double)ca + d * wB, (ca2 + cb2) + d * d * wAB);
+              } else {
+                ov[y] = (VT)((double)ca + d * wB);
+                o2[y] = (ca2 + cb2) + d * d * wAB;
+              }
             }
           } else {
             if (live) ov[y] = to_t<VT>(vop<K>((double)ca, (double)cb));
@@ -568,8 +605,14 @@ __global__ void __launch_bounds__(WTH, 3)
       for (int x = tid; x < E; x += WTH) {
         const int y = pad(x);
         t_out[ob + x] = st[y];
-        v_out[ob + x] = sv[y];
-        if (MOM) v2_out[ob + x] = s2[y];
+        if (P2) {
+          const double2 w = bp(cur)[y];
+          v_out[ob + x] = (VT)w.x;
+          v2_out[ob + x] = w.y;
+        } else {
+          v_out[ob + x] = sv[y];
+          if (MOM) v2_out[ob + x] = s2[y];
+        }
       }
     }
     // ---- next sub-window of the tile
