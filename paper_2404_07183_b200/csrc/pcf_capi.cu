@@ -123,6 +123,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
   static const bool kExactPartial = getenv("PCF_NO_EXACT_PARTIAL") == nullptr;
   static const bool kK1sEnabled = getenv("PCF_NO_K1S") == nullptr;
+  // per-item K1 configs (A/B: PCF_NO_ITEM_CONFIG=1 keeps the row block's config everywhere)
+  static const bool kPerItem = getenv("PCF_NO_ITEM_CONFIG") == nullptr;
   static const int kFastRingMinLogG =
       getenv("PCF_FAST_RING_MINLOG2G") ? atoi(getenv("PCF_FAST_RING_MINLOG2G")) : -1;
   // K1r merge-path split: with the column rings one lane per pair is fastest (c4 K1r
@@ -364,17 +366,62 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     const int64_t rows_pts = S[r0 + Rr] - S[r0];
     for (int64_t c0 = r0 + 1; c0 < c_end; c0 += span) {
       const int64_t c1 = std::min<int64_t>(c0 + span, c_end);
+      int i_logC = logC, i_logG = logG, i_mode = mode;
+      bool i_single = single;
+      if (kPerItem && (mode == 1 || mode == 4) && (r0 % GW) == 0) {
+        // per-item K1 config: the row block's config was sized on its FIRST columns (the
+        // longest: the sort is descending), but later items' columns are shorter, so more
+        // of them fit per chunk -- a smaller merge-path split G (fewer co-rank searches and
+        // partial sums per cell), or K1 instead of K1s for exact-mode items
+        const int lrg = Rr > GW ? 1 : 0;
+        const int64_t rows_b = group_recs(r0) * RB + (lrg ? group_recs(r0 + GW) * RB : 0);
+        for (int lc = LOGU - lrg; lc >= 0; --lc) {
+          const int lg = LOGU - lrg - lc;
+          if (lg > max_log2G) break;
+          const int64_t ce = std::min<int64_t>(c0 + ((int64_t)1 << lc), c1);
+          const int64_t need2 = al(rows_b) + 2 * al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
+          if (need2 > smem_budget) continue;
+          int nlc = lc, nlg = lg;
+          bool nsingle = false;
+          int64_t nneed = need2;
+          if (lg >= kSingleMinLogG) {  // as for the row block: one buffer of 2C halves G
+            const int64_t ce2 = std::min<int64_t>(c0 + ((int64_t)2 << lc), c1);
+            const int64_t need1 = al(rows_b) + al((S[ce2] - S[c0]) * RB + 32) + kRedBytes;
+            if (need1 <= smem_budget) {
+              nlc = lc + 1;
+              nlg = lg - 1;
+              nsingle = true;
+              nneed = need1;
+            }
+          }
+          // take it if it splits pairs less than the row block's config, keeps more lanes
+          // busy, or double-buffers at the same split (for a K1s row block: whenever a full
+          // 512-lane K1 config fits)
+          const bool better =
+              mode == 4 ? nlg == 0
+                        : (nlg < logG || (nlg == logG && nlc > logC) ||  // fewer splits / more lanes
+                           (nlg == logG && nlc == logC && single && !nsingle));  // 2 buffers
+          if (better) {
+            i_logC = nlc;
+            i_logG = nlg;
+            i_single = nsingle;
+            i_mode = 1;
+            need_max = std::max(need_max, nneed);
+          }
+          break;
+        }
+      }
       pcf_work_item w;
       w.row0 = (int32_t)r0;
       w.nrows = (int32_t)Rr;
       w.col0 = (int32_t)c0;
       w.col1 = (int32_t)c1;
-      w.logC = logC | (single ? 0x100 : 0) | (ring4 ? 0x200 : 0);
-      w.log2G = logG;
-      w.smem_mode = mode;
+      w.logC = i_logC | (i_single ? 0x100 : 0) | (ring4 ? 0x200 : 0);
+      w.log2G = i_logG;
+      w.smem_mode = i_mode;
       const double cells = (double)Rr * (double)(S[c1] - S[c0]) + (double)(c1 - c0) * rows_pts;
       w.cost_hi = (int32_t)std::min(2.0e9, cells / 1048576.0);
-      runs[mode == 1 ? 0 : (mode == 4 ? 2 : (mode == 2 ? 3 : 4))].push_back(w);
+      runs[i_mode == 1 ? 0 : (i_mode == 4 ? 2 : (i_mode == 2 ? 3 : 4))].push_back(w);
     }
     if (smem) need_max = std::max(need_max, best_need);
     r0 += Rr;
