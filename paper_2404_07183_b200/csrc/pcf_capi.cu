@@ -118,13 +118,24 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   const int T = kTileThreads;
   constexpr int64_t kK1rMinRecs = 1024;
   static const int kSingleMinLogG =
-      getenv("PCF_SINGLE_MIN_LOG2G") ? atoi(getenv("PCF_SINGLE_MIN_LOG2G")) : 3;
+      getenv("PCF_SINGLE_MIN_LOG2G") ? atoi(getenv("PCF_SINGLE_MIN_LOG2G")) : 1;
   // largest G accepted for single-buffered K1 on rows whose group misses double buffering
   static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
   static const bool kExactPartial = getenv("PCF_NO_EXACT_PARTIAL") == nullptr;
   static const bool kK1sEnabled = getenv("PCF_NO_K1S") == nullptr;
   // per-item K1 configs (A/B: PCF_NO_ITEM_CONFIG=1 keeps the row block's config everywhere)
   static const bool kPerItem = getenv("PCF_NO_ITEM_CONFIG") == nullptr;
+  // a single column buffer exposes one chunk copy per chunk; PCF_SINGLE_MIN_STEPS=n keeps
+  // double buffering unless each lane walks >= n cells per chunk (A/B: 256 made App-A 30k
+  // 437 -> 469 ms and c1/c2 no faster, so the default is 0 -- always halve G)
+  static const int kSingleMinSteps =
+      getenv("PCF_SINGLE_MIN_STEPS") ? atoi(getenv("PCF_SINGLE_MIN_STEPS")) : 0;
+  auto long_walk = [&](int64_t n_row, int64_t n_col, int lg_new) {
+    return ((n_row + n_col) >> std::max(lg_new, 0)) >= kSingleMinSteps;
+  };
+  // per-item single-buffer configs may take up to 2^kSingleMaxUp times the columns
+  static const int kSingleMaxUp =
+      getenv("PCF_SINGLE_MAX_UP") ? atoi(getenv("PCF_SINGLE_MAX_UP")) : 1;
   static const int kFastRingMinLogG =
       getenv("PCF_FAST_RING_MINLOG2G") ? atoi(getenv("PCF_FAST_RING_MINLOG2G")) : -1;
   // K1r merge-path split: with the column rings one lane per pair is fastest (c4 K1r
@@ -259,7 +270,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     if (use_ring) smem = false;
     int rows, logC, logG, s_mode = -1;
     bool ring4 = false;  // K1r: 4-slot column rings (flag bit 9 of logC)
-    if (smem && !single && best_logG >= kSingleMinLogG) {
+    if (smem && !single && best_logG >= kSingleMinLogG &&
+        long_walk(sizes[r0], sizes[std::min<int64_t>(r0 + 1, M - 1)], best_logG - 1)) {
       // long rows: G >= 16 merge-path segments of a few dozen steps each.  A single
       // column buffer of twice the columns halves G (half the co-rank searches and
       // partial sums per cell) at the price of one exposed chunk load per chunk.
@@ -384,14 +396,20 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
           int nlc = lc, nlg = lg;
           bool nsingle = false;
           int64_t nneed = need2;
-          if (lg >= kSingleMinLogG) {  // as for the row block: one buffer of 2C halves G
-            const int64_t ce2 = std::min<int64_t>(c0 + ((int64_t)2 << lc), c1);
-            const int64_t need1 = al(rows_b) + al((S[ce2] - S[c0]) * RB + 32) + kRedBytes;
-            if (need1 <= smem_budget) {
-              nlc = lc + 1;
-              nlg = lg - 1;
-              nsingle = true;
-              nneed = need1;
+          if (lg >= kSingleMinLogG && long_walk(sizes[r0], sizes[c0], lg - 1)) {
+            // one column buffer instead of two: the most columns that fit (2C, 4C, ...)
+            // divide G accordingly, at the price of one exposed chunk copy per chunk
+            for (int up = kSingleMaxUp; up >= 1; --up) {
+              if (lg - up < 0) continue;
+              const int64_t ce2 = std::min<int64_t>(c0 + ((int64_t)1 << (lc + up)), c1);
+              const int64_t need1 = al(rows_b) + al((S[ce2] - S[c0]) * RB + 32) + kRedBytes;
+              if (need1 <= smem_budget) {
+                nlc = lc + up;
+                nlg = lg - up;
+                nsingle = true;
+                nneed = need1;
+                break;
+              }
             }
           }
           // take it if it splits pairs less than the row block's config, keeps more lanes
