@@ -21,13 +21,14 @@ arithmetic in 64-bit, pyx:38-41); results are rounded back to float32 at the end
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
 from . import _native, errors
 
 _SMEM_BUDGET = 220 * 1024
-_MAX_COLS_PER_ITEM = 2048
+_MAX_COLS_PER_ITEM = int(os.environ.get("PCF_MAX_COLS", "2048"))  # columns per work item (A/B knob)
 
 
 def _torch():

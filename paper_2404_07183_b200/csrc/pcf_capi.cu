@@ -123,6 +123,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   static const bool kK1cEnabled = getenv("PCF_NO_K1C") == nullptr;
   static const bool kExactPartial = getenv("PCF_NO_EXACT_PARTIAL") == nullptr;
   static const bool kK1sEnabled = getenv("PCF_NO_K1S") == nullptr;
+  // at equal G, one 8-row group with twice the columns instead of two groups (A/B knob)
+  static const bool kPreferRG1 = getenv("PCF_PREFER_RG1") != nullptr;
   // per-item K1 configs (A/B: PCF_NO_ITEM_CONFIG=1 keeps the row block's config everywhere)
   static const bool kPerItem = getenv("PCF_NO_ITEM_CONFIG") == nullptr;
   // a single column buffer exposes one chunk copy per chunk; PCF_SINGLE_MIN_STEPS=n keeps
@@ -203,7 +205,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
         const int64_t need =
             al(rows_b) + 2 * al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
         if (need > smem_budget) continue;
-        if (logG < best_logG || (logG == best_logG && logRG > best_logRG)) {
+        if (logG < best_logG ||
+            (logG == best_logG && (kPreferRG1 ? logRG < best_logRG : logRG > best_logRG))) {
           best_logRG = logRG;
           best_logC = logC;
           best_logG = logG;
