@@ -127,6 +127,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   static const bool kPreferRG1 = getenv("PCF_PREFER_RG1") != nullptr;
   // per-item K1 configs (A/B: PCF_NO_ITEM_CONFIG=1 keeps the row block's config everywhere)
   static const bool kPerItem = getenv("PCF_NO_ITEM_CONFIG") == nullptr;
+  static const bool kExactSingle = getenv("PCF_NO_EXACT_SINGLE") == nullptr;
   // a single column buffer exposes one chunk copy per chunk; PCF_SINGLE_MIN_STEPS=n keeps
   // double buffering unless each lane walks >= n cells per chunk (A/B: 256 made App-A 30k
   // 437 -> 469 ms and c1/c2 no faster, so the default is 0 -- always halve G)
@@ -430,6 +431,20 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
             need_max = std::max(need_max, nneed);
           }
           break;
+        }
+        if (max_log2G == 0 && kExactSingle && !(i_mode == 1 && i_logC == LOGU - lrg)) {
+          // exact mode: a full 512-lane K1 chunk (64 / RG columns) in ONE buffer, where two
+          // do not fit -- K1 instead of K1s, or all lanes instead of K1's idle quarters
+          const int lc = LOGU - lrg;
+          const int64_t ce = std::min<int64_t>(c0 + ((int64_t)1 << lc), c1);
+          const int64_t need1 = al(rows_b) + al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
+          if (need1 <= smem_budget) {
+            i_logC = lc;
+            i_logG = 0;
+            i_single = true;
+            i_mode = 1;
+            need_max = std::max(need_max, need1);
+          }
         }
       }
       pcf_work_item w;
