@@ -27,7 +27,9 @@ import numpy as np
 
 from . import _native, errors
 
-_SMEM_BUDGET = 220 * 1024
+# the sm_100 opt-in dynamic shared-memory maximum (227 KB) less the tile kernels' static
+# shared memory (csrc/pcf_internal.h kPlanSmemBudget); PCF_SMEM_BUDGET overrides (A/B)
+_SMEM_BUDGET = int(os.environ.get("PCF_SMEM_BUDGET", str(227 * 1024 - 64)))
 _MAX_COLS_PER_ITEM = int(os.environ.get("PCF_MAX_COLS", "2048"))  # columns per work item (A/B knob)
 
 

@@ -361,11 +361,11 @@ int pcf_matrix_host(const void* tcat, const void* vcat, int is_f32, const int64_
   // one planner pass into a generous buffer (App-A 100k: 2.5 items per PCF); a second
   // pass only if it was too small
   std::vector<pcf_work_item> items((size_t)std::max<int64_t>(1024, 4 * M));
-  rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, max_cols, max_log2G, rec_bytes, items.data(),
+  rc = pcf_plan_pairwise(ss.data(), M, kPlanSmemBudget, max_cols, max_log2G, rec_bytes, items.data(),
                          (int64_t)items.size(), &n_items, &smem);
   if (rc == PCF_ERR_ARG && n_items > (int64_t)items.size()) {
     items.resize((size_t)n_items);
-    rc = pcf_plan_pairwise(ss.data(), M, 220 * 1024, max_cols, max_log2G, rec_bytes,
+    rc = pcf_plan_pairwise(ss.data(), M, kPlanSmemBudget, max_cols, max_log2G, rec_bytes,
                            items.data(), n_items, &n_items, &smem);
   }
   if (rc) return cudaStreamSynchronize(s0), rc;

@@ -5,6 +5,10 @@
 #include "../../include/pcf_b200.h"
 
 namespace pcfb {
+// dynamic shared memory the pairwise planner may give one tile CTA: the sm_100 opt-in
+// maximum (227 KB) less the tile kernels' static shared memory (A/B at App-A 30k: 220 KB
+// -> 227 KB, fast 437 -> 434 ms, exact 581 -> 579 ms)
+constexpr int64_t kPlanSmemBudget = 227 * 1024 - 64;
 
 constexpr int kTileThreads = 512;  // CTA size of the persistent tile kernels
 // K1s column prefetch ring: slots per lane (pcf_tiles.cuh kRingSlots); the ring takes

@@ -124,11 +124,11 @@ int get_plan(Collection& C, int lg, Plan** out) {
   int64_t n = 0;
   const int rb = C.is_f32 ? 8 : 16;
   P.items.resize((size_t)std::max<int64_t>(1024, 4 * C.M));
-  int rc = pcf_plan_pairwise(C.ss.data(), C.M, 220 * 1024, 2048, lg, rb, P.items.data(),
+  int rc = pcf_plan_pairwise(C.ss.data(), C.M, kPlanSmemBudget, 2048, lg, rb, P.items.data(),
                              (int64_t)P.items.size(), &n, &P.smem);
   if (rc == PCF_ERR_ARG && n > (int64_t)P.items.size()) {
     P.items.resize((size_t)n);
-    rc = pcf_plan_pairwise(C.ss.data(), C.M, 220 * 1024, 2048, lg, rb, P.items.data(), n, &n,
+    rc = pcf_plan_pairwise(C.ss.data(), C.M, kPlanSmemBudget, 2048, lg, rb, P.items.data(), n, &n,
                            &P.smem);
   }
   if (rc) return rc;

@@ -94,8 +94,10 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
             al = lambda x: (x + 127) // 128 * 128  # noqa: E731
             nbuf = 1 if single else 2
             assert al(rows_b) + nbuf * al(col_b) + 4 * 512 * 8 <= smem <= 220 * 1024
-            if single and G > 1:  # only where the double-buffered split would be G >= 8
-                assert G >= 4
+            if single and G > 1:
+                # one buffer of 2C columns replaces two of C / 2 (split 2G), which fit
+                half_c = (S[min(col0 + C // 2, col1)] - S[col0]) * rec_bytes + 32
+                assert al(rows_b) + 2 * al(half_c) + 4 * 512 * 8 <= 220 * 1024
         elif mode == 3:  # K1c: one resident row x interleaved column groups (CG x G units)
             assert nrows == 1 and C * G == units
             gs = [gw * sizes[gw * k] * rec_bytes for k in range(col0 // gw,
