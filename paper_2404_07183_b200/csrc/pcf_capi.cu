@@ -136,6 +136,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   auto long_walk = [&](int64_t n_row, int64_t n_col, int lg_new) {
     return ((n_row + n_col) >> std::max(lg_new, 0)) >= kSingleMinSteps;
   };
+  static const bool kRedOnlyG = getenv("PCF_RED_ALWAYS") == nullptr;
+  auto red_bytes = [&](int lg) -> int64_t { return (lg > 0 || !kRedOnlyG) ? kRedBytes : 0; };
   // per-item single-buffer configs may take up to 2^kSingleMaxUp times the columns
   static const int kSingleMaxUp =
       getenv("PCF_SINGLE_MAX_UP") ? atoi(getenv("PCF_SINGLE_MAX_UP")) : 1;
@@ -395,7 +397,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
           const int lg = LOGU - lrg - lc;
           if (lg > max_log2G) break;
           const int64_t ce = std::min<int64_t>(c0 + ((int64_t)1 << lc), c1);
-          const int64_t need2 = al(rows_b) + 2 * al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
+          // (the segment partials area is only touched when G > 1)
+          const int64_t need2 = al(rows_b) + 2 * al((S[ce] - S[c0]) * RB + 32) + red_bytes(lg);
           if (need2 > smem_budget) continue;
           int nlc = lc, nlg = lg;
           bool nsingle = false;
@@ -406,7 +409,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
             for (int up = kSingleMaxUp; up >= 1; --up) {
               if (lg - up < 0) continue;
               const int64_t ce2 = std::min<int64_t>(c0 + ((int64_t)1 << (lc + up)), c1);
-              const int64_t need1 = al(rows_b) + al((S[ce2] - S[c0]) * RB + 32) + kRedBytes;
+              const int64_t need1 = al(rows_b) + al((S[ce2] - S[c0]) * RB + 32) + red_bytes(lg - up);
               if (need1 <= smem_budget) {
                 nlc = lc + up;
                 nlg = lg - up;
@@ -437,7 +440,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
           // do not fit -- K1 instead of K1s, or all lanes instead of K1's idle quarters
           const int lc = LOGU - lrg;
           const int64_t ce = std::min<int64_t>(c0 + ((int64_t)1 << lc), c1);
-          const int64_t need1 = al(rows_b) + al((S[ce] - S[c0]) * RB + 32) + kRedBytes;
+          const int64_t need1 = al(rows_b) + al((S[ce] - S[c0]) * RB + 32) + red_bytes(0);
           if (need1 <= smem_budget) {
             i_logC = lc;
             i_logG = 0;

@@ -93,7 +93,8 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
             col_b = (S[min(col0 + C, col1)] - S[col0]) * rec_bytes + 32
             al = lambda x: (x + 127) // 128 * 128  # noqa: E731
             nbuf = 1 if single else 2
-            assert al(rows_b) + nbuf * al(col_b) + 4 * 512 * 8 <= smem <= 220 * 1024
+            red = 4 * 512 * 8 if G > 1 else 0  # segment partials: only split pairs use them
+            assert al(rows_b) + nbuf * al(col_b) + red <= smem <= 220 * 1024
             if single and G > 1:
                 # one buffer of 2C columns replaces two of C / 2 (split 2G), which fit
                 half_c = (S[min(col0 + C // 2, col1)] - S[col0]) * rec_bytes + 32
