@@ -128,6 +128,8 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   // per-item K1 configs (A/B: PCF_NO_ITEM_CONFIG=1 keeps the row block's config everywhere)
   static const bool kPerItem = getenv("PCF_NO_ITEM_CONFIG") == nullptr;
   static const bool kExactSingle = getenv("PCF_NO_EXACT_SINGLE") == nullptr;
+  // K1s with one 8-row group (80 columns per pass) even where two fit (A/B knob)
+  static const bool kK1sRG1 = getenv("PCF_K1S_RG1") != nullptr;
   // a single column buffer exposes one chunk copy per chunk; PCF_SINGLE_MIN_STEPS=n keeps
   // double buffering unless each lane walks >= n cells per chunk (A/B: 256 made App-A 30k
   // 437 -> 469 ms and c1/c2 no faster, so the default is 0 -- always halve G)
@@ -321,7 +323,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       // prefetch ring, 64 quarters = RG x C columns per pass
       int64_t rows_b = group_recs(r0) * RB;
       int lrg = 0;
-      if (r0 + GW < M - 1 &&
+      if (!kK1sRG1 && r0 + GW < M - 1 &&
           al(rows_b + group_recs(r0 + GW) * RB) + k1s_ring <= smem_budget) {
         rows_b += group_recs(r0 + GW) * RB;
         lrg = 1;
