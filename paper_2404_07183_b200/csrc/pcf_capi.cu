@@ -139,7 +139,11 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
     return ((n_row + n_col) >> std::max(lg_new, 0)) >= kSingleMinSteps;
   };
   static const bool kRedOnlyG = getenv("PCF_RED_ALWAYS") == nullptr;
-  auto red_bytes = [&](int lg) -> int64_t { return (lg > 0 || !kRedOnlyG) ? kRedBytes : 0; };
+  // K1 segment partials: [2][512] doubles plus [2][512 / G] tails, only when G > 1
+  auto red_bytes = [&](int lg) -> int64_t {
+    if (!kRedOnlyG) return kRedBytes;
+    return lg > 0 ? (int64_t)(2 * kTileThreads + 2 * (kTileThreads >> lg)) * 8 : 0;
+  };
   // per-item single-buffer configs may take up to 2^kSingleMaxUp times the columns
   static const int kSingleMaxUp =
       getenv("PCF_SINGLE_MAX_UP") ? atoi(getenv("PCF_SINGLE_MAX_UP")) : 1;

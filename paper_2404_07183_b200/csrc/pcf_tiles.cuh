@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     unsigned char* colbase = smem + row_al;  // column buffer k at colbase + k * col_al
     const int ncb = single ? 1 : 2;  // column buffers
     double* red = reinterpret_cast<double*>(smem + row_al + ncb * col_al);  // [2][512] partials
-    double* redh = red + 2 * kTileThreads;                                   // [2][pairs] tails
+    double* redh = red + 2 * kTileThreads;  // [2][npairs] tails (npairs = 512 / G)
     // issue chunk c into its column buffer (thread 0)
     auto issue = [&](int c) {
       const int cb = W.col0 + (c << logC), ce = min(cb + C, W.col1);
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         if (tid == 0 && c + ncb < nchunk) issue(c + ncb);
       } else {
         red[buf * kTileThreads + g * npairs + pair_id] = acc;  // segment-major: no conflicts
-        if (g == 0) redh[buf * kTileThreads + pair_id] = hl;
+        if (g == 0) redh[buf * npairs + pair_id] = hl;
         __syncthreads();  // partials visible, column buffer `kb` free again
         if (tid == 0 && c + ncb < nchunk) issue(c + ncb);  // before finishing: keep TMA busy
         if (tid < npairs) {
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             const double* r = red + buf * kTileThreads + tid;
             double s = r[0];
             for (int k = 1; k < G; ++k) s = __dadd_rn(s, r[k * npairs]);
-            finish_entry<HK, BOUNDED, OutT>(s, redh[buf * kTileThreads + tid], p, apply_root,
+            finish_entry<HK, BOUNDED, OutT>(s, redh[buf * npairs + tid], p, apply_root,
                                         fpi, pq, out, ld, M, err);
           }
         }
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     unsigned char* rowbuf = smem;
     unsigned char* colbase = smem + row_al;
     double* red = reinterpret_cast<double*>(smem + row_al + ncb * col_al);  // [2][512] partials
-    double* redh = red + 2 * kTileThreads;                                   // [2][pairs] tails
+    double* redh = red + 2 * kTileThreads;  // [2][npairs] tails (npairs = 512 / G)
     auto issue = [&](int c) {
       const int kb0 = gk0 + (c << logCG), kb1 = min(kb0 + CG, gk1);
       const uint32_t nb = (uint32_t)((goff[kb1] - goff[kb0]) * sizeof(RT));
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         if (tid == 0 && c + ncb < nchunk) issue(c + ncb);
       } else {
         red[buf * kTileThreads + g * npairs + pair_id] = acc;
-        if (g == 0) redh[buf * kTileThreads + pair_id] = hl;
+        if (g == 0) redh[buf * npairs + pair_id] = hl;
         __syncthreads();
         if (tid == 0 && c + ncb < nchunk) issue(c + ncb);
         if (tid < npairs) {
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             const double* r = red + buf * kTileThreads + tid;
             double sacc = r[0];
             for (int kk = 1; kk < G; ++kk) sacc = __dadd_rn(sacc, r[kk * npairs]);
-            finish_entry<HK, BOUNDED, OutT>(sacc, redh[buf * kTileThreads + tid], p, apply_root,
+            finish_entry<HK, BOUNDED, OutT>(sacc, redh[buf * npairs + tid], p, apply_root,
                                         oi, perm[pqs], out, ld, M, err);
           }
         }

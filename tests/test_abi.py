@@ -93,12 +93,13 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
             col_b = (S[min(col0 + C, col1)] - S[col0]) * rec_bytes + 32
             al = lambda x: (x + 127) // 128 * 128  # noqa: E731
             nbuf = 1 if single else 2
-            red = 4 * 512 * 8 if G > 1 else 0  # segment partials: only split pairs use them
+            # segment partials [2][512] + tails [2][512 / G]: only split pairs use them
+            red = (2 * 512 + 2 * (512 // G)) * 8 if G > 1 else 0
             assert al(rows_b) + nbuf * al(col_b) + red <= smem <= 220 * 1024
             if single and G > 1:
                 # one buffer of 2C columns replaces two of C / 2 (split 2G), which fit
                 half_c = (S[min(col0 + C // 2, col1)] - S[col0]) * rec_bytes + 32
-                assert al(rows_b) + 2 * al(half_c) + 4 * 512 * 8 <= 220 * 1024
+                assert al(rows_b) + 2 * al(half_c) + (2 * 512 + 2 * (512 // (2 * G))) * 8 <= 220 * 1024
         elif mode == 3:  # K1c: one resident row x interleaved column groups (CG x G units)
             assert nrows == 1 and C * G == units
             gs = [gw * sizes[gw * k] * rec_bytes for k in range(col0 // gw,
