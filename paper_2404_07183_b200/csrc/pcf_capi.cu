@@ -166,6 +166,12 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
   // K1c (one long row resident, interleaved column groups streamed): the best config for a
   // column range starting at group ks -- largest CG (fewest segments) that fits, double
   // buffered if possible.  Returns false if not even one group fits.
+  // K1c segment partials as K1's: [2][512] + tails [2][512 / G], nothing without a split
+  static const bool kK1cRedFull = getenv("PCF_RED_ALWAYS") != nullptr;
+  auto k1c_red = [&](int g) -> int64_t {
+    if (kK1cRedFull) return kRedBytes;
+    return g > 0 ? (int64_t)(2 * kTileThreads + 2 * (kTileThreads >> g)) * 8 : 0;
+  };
   auto k1c_config = [&](int64_t r, int64_t ks, int* lcg, int* lg, bool* one, int64_t* need) {
     const int64_t row_need = al((sizes[r] + 4) * RB + 16);
     for (int l = LOGU; l >= 0; --l) {
@@ -175,7 +181,7 @@ int pcf_plan_pairwise(const int64_t* sizes, int64_t M, int64_t smem_budget, int6
       int64_t chunk = 0;
       for (int64_t k = ks; k < ke; ++k) chunk += group_recs(GW * k) * RB;
       for (int nb = 2; nb >= 1; --nb) {
-        const int64_t nd = row_need + nb * al(chunk + 16) + kRedBytes;
+        const int64_t nd = row_need + nb * al(chunk + 16) + k1c_red(g);
         if (nd <= smem_budget) {
           *lcg = l;
           *lg = g;

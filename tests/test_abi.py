@@ -106,7 +106,8 @@ def test_planner_covers_upper_triangle_once(dist, max_log2g, rec_bytes):
                                                                min((col0 // gw) + C, (M + gw - 1) // gw))]
             al = lambda x: (x + 127) // 128 * 128  # noqa: E731
             nbuf = 1 if single else 2
-            assert al((sizes[row0] + 4) * rec_bytes + 16) + nbuf * al(sum(gs) + 16) + 4 * 512 * 8 \
+            red = (2 * 512 + 2 * (512 // G)) * 8 if G > 1 else 0
+            assert al((sizes[row0] + 4) * rec_bytes + 16) + nbuf * al(sum(gs) + 16) + red \
                 <= smem <= 220 * 1024
         elif mode == 2:  # K1r: one resident row, C columns x G segments
             assert nrows == 1 and C * G == threads and G <= 32
